@@ -1,0 +1,189 @@
+/*
+ * lagtrans_b200.h — C ABI of liblagtrans_b200.so, the B200 drop-in for the
+ * particle time step of the reference `lagtrans` package
+ * (/root/reference/pkg/src/lagtrans).
+ *
+ * The reference has no native layer: its hot path is reached through three
+ * Python surfaces, and every entry point below replaces one
+ * of them.  Citations are reference file:line.
+ *
+ *   module API    physics.module_*(ctl, ens, met0, met1, dt, [rnd], [cache], work)
+ *                 physics.py:82-301            -> lt_run (one module bit each)
+ *   RNG API       rng.generate_random_nums      rng.py:156-181 -> lt_rng_fill
+ *   runtime API   DevicePool.region_create / region_update_device /
+ *                 region_update_host / region_delete / device_wait
+ *                 device_runtime.py:165-230,118-127
+ *                 -> lt_ctx_create / lt_particles_alloc / lt_field_h2d /
+ *                    lt_met_load / lt_field_d2h / lt_ctx_destroy / lt_sync
+ *
+ * Conventions
+ *   - Every function returns an int status: LT_OK (0) or a negative code;
+ *     lt_last_error() gives the message of the calling thread's last failure.
+ *     The Python layer maps codes onto the reference exception types
+ *     (ValueError, IndexError, device_runtime.LifecycleError, RuntimeError).
+ *   - No function throws; no torch types appear in any signature.
+ *   - Host arrays are borrowed for the duration of the call only and must be
+ *     C-contiguous.  Copies into device memory are ordered on the context's
+ *     compute stream; D2H copies return after the data has landed.
+ *   - One context per GPU; a context is driven by one host thread at a time
+ *     (the DevicePool worker model, device_runtime.py:100-102).
+ */
+#ifndef LAGTRANS_B200_H
+#define LAGTRANS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LT_ABI_VERSION 1
+
+/* status codes */
+#define LT_OK 0
+#define LT_ERR_ARG (-1)    /* invalid argument          -> ValueError      */
+#define LT_ERR_RANGE (-2)  /* work range out of bounds  -> IndexError      */
+#define LT_ERR_STATE (-3)  /* lifecycle violation       -> LifecycleError  */
+#define LT_ERR_CUDA (-4)   /* CUDA failure              -> RuntimeError    */
+#define LT_ERR_NOMEM (-5)  /* device allocation failed  -> MemoryError     */
+
+/* module bits for lt_run (pipeline order driver_cli.py:31-33; decay is new) */
+#define LT_MOD_TIMESTEPS    (1u << 0)  /* physics.py:82-88   */
+#define LT_MOD_ADVECTION    (1u << 1)  /* physics.py:91-116  */
+#define LT_MOD_TURB         (1u << 2)  /* physics.py:119-147 */
+#define LT_MOD_MESO         (1u << 3)  /* physics.py:150-188 */
+#define LT_MOD_CONVECTION   (1u << 4)  /* physics.py:191-203 */
+#define LT_MOD_SEDI         (1u << 5)  /* physics.py:206-222 */
+#define LT_MOD_DECAY        (1u << 6)  /* new: exponential decay of q[decay_slot] */
+#define LT_MOD_ISOSURF      (1u << 7)  /* physics.py:238-264 */
+#define LT_MOD_POSITION     (1u << 8)  /* physics.py:267-287 */
+#define LT_MOD_METEO        (1u << 9)  /* physics.py:290-301 */
+#define LT_MOD_ISOSURF_INIT (1u << 10) /* physics.py:225-235 */
+
+/* lt_run flags */
+#define LT_RUN_RNG_INKERNEL (1u << 0) /* draw randoms in-kernel (else read the batch) */
+#define LT_RUN_DT_ARRAY     (1u << 1) /* read dt from the dt array (else inline)       */
+#define LT_RUN_WRITE_DT     (1u << 2) /* store dt computed by TIMESTEPS               */
+
+/* rng modes (model_state.py:15 plus the fast Philox mode) */
+#define LT_RNG_FAITHFUL 0
+#define LT_RNG_COUNTER 1
+#define LT_RNG_PHILOX 2
+
+/* isosurface modes (model_state.py:14) */
+#define LT_ISO_OFF 0
+#define LT_ISO_PRESSURE 1
+#define LT_ISO_THETA 2
+
+/* per-particle fields (ParticleEnsemble model_state.py:92-110,
+   CacheState :184-195, dt, RandomBatch rng.py:32-44) */
+#define LT_F_TIME 0
+#define LT_F_P 1
+#define LT_F_ZETA 2
+#define LT_F_LON 3
+#define LT_F_LAT 4
+#define LT_F_Q 5        /* row = quantity slot 0..nq-1            */
+#define LT_F_UVWP 6     /* row = component 0..2                   */
+#define LT_F_ISO_VAR 7
+#define LT_F_DT 8
+#define LT_F_RND_CONV 9 /* n doubles                              */
+#define LT_F_RND_TURB 10 /* 3n doubles, [3i:3i+3] for particle i  */
+#define LT_F_RND_MESO 11 /* 3n doubles                            */
+#define LT_F_ID 12      /* uint32 global particle index (sorted layouts) */
+
+/* met storage precision for lt_met_grid */
+#define LT_MET_F32 4
+#define LT_MET_F64 8
+/* lt_met_load flags */
+#define LT_MET_CLOSE_LON (1u << 0) /* source lacks the +360 column: append column 0
+                                      (ingest.py:195-207 met_periodic) */
+#define LT_MET_DEVICE_SRC (1u << 1) /* source pointers are device memory (e.g. an
+                                       NCCL-broadcast buffer): pack without staging */
+
+/* kernel-relevant Control fields (model_state.py:18-45) + decay */
+typedef struct lt_control {
+  double t_stop, dt_model, met_dt;
+  double turb_dx, turb_dz, turb_meso;
+  double conv_prob, conv_p_top, p_surf, p_top;
+  double sedi_radius, sedi_density;
+  double decay_tau;          /* s, <= 0 disables */
+  int32_t isosurf_mode;      /* LT_ISO_*  */
+  int32_t rng_mode;          /* LT_RNG_*  */
+  uint64_t rng_seed_global;  /* counter / philox key */
+  int32_t decay_slot;        /* q row decayed by LT_MOD_DECAY */
+  int32_t reserved;
+} lt_control;
+
+typedef struct lt_ctx lt_ctx;
+
+/* library / device discovery (device_runtime.py:39-55) */
+int lt_abi_version(void);
+int lt_device_count(int32_t *n);
+const char *lt_last_error(void);
+
+/* context = one GPU's data region (device_runtime.py:165-186) */
+int lt_ctx_create(int32_t device, lt_ctx **out);
+int lt_ctx_destroy(lt_ctx *ctx);                  /* region_delete */
+int lt_sync(lt_ctx *ctx);                         /* device_wait   */
+int lt_stream(lt_ctx *ctx, void **cuda_stream);   /* interop       */
+
+/* particle store: SoA in HBM, `capacity` particles, nq quantity rows */
+int lt_particles_alloc(lt_ctx *ctx, int64_t capacity, int32_t nq, int32_t with_batch);
+int lt_field_h2d(lt_ctx *ctx, int32_t field, int32_t row, int64_t offset,
+                 int64_t count, const void *host);
+int lt_field_d2h(lt_ctx *ctx, int32_t field, int32_t row, int64_t offset,
+                 int64_t count, void *host);
+int lt_field_fill(lt_ctx *ctx, int32_t field, int32_t row, int64_t offset,
+                  int64_t count, double value);
+int lt_field_devptr(lt_ctx *ctx, int32_t field, int32_t row, void **dev);
+int lt_ids_reset(lt_ctx *ctx, int64_t offset, int64_t count, int64_t first_id);
+
+/* met store: up to 3 snapshot slots on one grid (MeteoField model_state.py:126-153) */
+int lt_met_grid(lt_ctx *ctx, int32_t nx, int32_t ny, int32_t nz, const double *lons,
+                const double *lats, const double *levs, int32_t precision);
+int lt_met_load(lt_ctx *ctx, int32_t slot, double t_met, int32_t src_bytes,
+                const void *u, const void *v, const void *w, const void *T,
+                uint32_t flags);
+int lt_met_load_nodes(lt_ctx *ctx, int32_t slot, double t_met, const float *uvwT,
+                      uint32_t flags);
+int lt_met_use(lt_ctx *ctx, int32_t slot0, int32_t slot1);
+int lt_met_slot_time(lt_ctx *ctx, int32_t slot, double *t_met);
+
+/* climatology tables for module_meteo (ClimData model_state.py:156-181) */
+int lt_clim_load(lt_ctx *ctx, int32_t nlat, int32_t np_, const double *lat_grid,
+                 const double *p_grid, const double *hno3, const double *p_trop);
+
+/* compute: apply the modules in `modules` to particles [start, end) */
+int lt_run(lt_ctx *ctx, const lt_control *ctl, uint32_t modules, int64_t start,
+           int64_t end, int64_t step, uint64_t faithful_state,
+           int64_t faithful_base, uint32_t flags);
+/* fill the device RandomBatch for [start, end) (rng.py:156-181) */
+int lt_rng_fill(lt_ctx *ctx, int32_t mode, uint64_t seed_or_state, int64_t step,
+                int64_t start, int64_t end);
+/* interpolate_met (physics.py:69-79) at n host points: out = u,v,w,T rows (4n) */
+int lt_interpolate(lt_ctx *ctx, int64_t n, const double *t, const double *lon,
+                   const double *lat, const double *p, double *out);
+/* theta-isosurface non-convergence counter (CacheState.iso_nonconverged) */
+int lt_iso_counter(lt_ctx *ctx, int64_t *value, int32_t reset);
+
+/* box sort: stable radix sort of [start, end) by met0 cell, ids travel along */
+int lt_sort_by_box(lt_ctx *ctx, int64_t start, int64_t end);
+/* copies that undo the sort permutation (ids must be a permutation of
+   [first_id, first_id + count)) */
+int lt_field_d2h_ordered(lt_ctx *ctx, int32_t field, int32_t row, int64_t offset,
+                         int64_t count, int64_t first_id, void *host);
+int lt_field_h2d_ordered(lt_ctx *ctx, int32_t field, int32_t row, int64_t offset,
+                         int64_t count, int64_t first_id, const void *host);
+
+/* event timing of the last lt_run / lt_sort_by_box on this context */
+int lt_timing(lt_ctx *ctx, int32_t enable);
+int lt_last_elapsed_ms(lt_ctx *ctx, float *ms);
+
+/* pinned host memory for streaming met snapshots */
+int lt_host_alloc(int64_t bytes, void **out);
+int lt_host_free(void *p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LAGTRANS_B200_H */

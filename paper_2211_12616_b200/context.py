@@ -1,0 +1,237 @@
+"""DeviceContext — one GPU's data region, a thin owner of an `lt_ctx`.
+
+Equivalent of one DevicePool worker's ModelImage in the reference
+(device_runtime.py:58-69,165-230), but resident in HBM: SoA particle
+fields, up to three met snapshot slots, climatology tables and the CUDA
+streams, all owned by liblagtrans_b200.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import hashlib
+
+import numpy as np
+
+from . import _capi as capi
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def met_fingerprint(met) -> tuple:
+    """Cheap identity of a MeteoField's content: object ids, shapes, time and
+    a hash of a strided sample of every field (full bytes when small)."""
+    h = hashlib.blake2b(digest_size=16)
+    for name in ("lons", "lats", "levs", "u", "v", "w", "T"):
+        a = np.asarray(getattr(met, name))
+        h.update(str(a.shape).encode())
+        flat = a.reshape(-1)
+        if flat.size > (1 << 20):
+            flat = flat[:: flat.size // 65536 + 1]
+        h.update(np.ascontiguousarray(flat).tobytes())
+    return (float(met.t_met), h.hexdigest())
+
+
+class DeviceContext:
+    """Owns one lt_ctx on `device`; all methods raise the reference's
+    exception types on failure (ValueError, IndexError, LifecycleError)."""
+
+    def __init__(self, device: int = 0, met_precision: str = "f32"):
+        self.lib = capi.load()
+        self.device = device
+        h = C.c_void_p()
+        capi.check(self.lib.lt_ctx_create(device, C.byref(h)))
+        self.h = h
+        self.capacity = 0
+        self.nq = 0
+        self.with_batch = False
+        self.met_precision = met_precision
+        self._grid_key = None
+        self._slot_keys = [None, None, None]
+        self._clim_key = None
+        self.closed = False
+
+    # -- lifecycle -------------------------------------------------------
+    def close(self) -> None:
+        if not self.closed:
+            self.closed = True
+            capi.check(self.lib.lt_ctx_destroy(self.h))
+
+    def __del__(self):  # best effort
+        try:
+            if not self.closed:
+                self.lib.lt_ctx_destroy(self.h)
+                self.closed = True
+        except Exception:
+            pass
+
+    def sync(self) -> None:
+        capi.check(self.lib.lt_sync(self.h))
+
+    def stream_handle(self) -> int:
+        s = C.c_void_p()
+        capi.check(self.lib.lt_stream(self.h, C.byref(s)))
+        return s.value or 0
+
+    # -- particles -------------------------------------------------------
+    def alloc(self, capacity: int, nq: int = 5, with_batch: bool = False) -> None:
+        capi.check(self.lib.lt_particles_alloc(self.h, int(capacity), int(nq), int(with_batch)))
+        self.capacity, self.nq, self.with_batch = int(capacity), int(nq), bool(with_batch)
+
+    def ensure_capacity(self, n: int, nq: int = 5, with_batch: bool = False) -> None:
+        if n > self.capacity or nq > self.nq or (with_batch and not self.with_batch) \
+                or self.capacity == 0:
+            self.alloc(max(n, 1), max(nq, 5), with_batch or self.with_batch)
+
+    def h2d(self, field: int, row: int, offset: int, arr) -> None:
+        a = _f64(arr)
+        capi.check(self.lib.lt_field_h2d(self.h, field, row, offset, a.size, capi.ptr(a)))
+
+    def d2h(self, field: int, row: int, offset: int, count: int, out=None) -> np.ndarray:
+        out = np.empty(count) if out is None else out
+        capi.check(self.lib.lt_field_d2h(self.h, field, row, offset, count, capi.ptr(out)))
+        return out
+
+    def h2d_ordered(self, field, row, offset, arr, first_id) -> None:
+        a = _f64(arr)
+        capi.check(self.lib.lt_field_h2d_ordered(self.h, field, row, offset, a.size, first_id,
+                                                 capi.ptr(a)))
+
+    def d2h_ordered(self, field, row, offset, count, first_id, out=None) -> np.ndarray:
+        out = np.empty(count) if out is None else out
+        capi.check(self.lib.lt_field_d2h_ordered(self.h, field, row, offset, count, first_id,
+                                                 capi.ptr(out)))
+        return out
+
+    def fill(self, field, row, offset, count, value) -> None:
+        capi.check(self.lib.lt_field_fill(self.h, field, row, offset, count, float(value)))
+
+    def ids(self, offset: int, count: int) -> np.ndarray:
+        out = np.empty(count, dtype=np.uint32)
+        capi.check(self.lib.lt_field_d2h(self.h, capi.F_ID, 0, offset, count, capi.ptr(out)))
+        return out
+
+    def ids_reset(self, offset: int, count: int, first_id: int) -> None:
+        capi.check(self.lib.lt_ids_reset(self.h, offset, count, first_id))
+
+    def devptr(self, field: int, row: int = 0) -> int:
+        p = C.c_void_p()
+        capi.check(self.lib.lt_field_devptr(self.h, field, row, C.byref(p)))
+        return p.value or 0
+
+    # -- met ---------------------------------------------------------------
+    def set_grid(self, lons, lats, levs, precision: str | None = None) -> None:
+        prec = precision or self.met_precision
+        lons, lats, levs = _f64(lons), _f64(lats), _f64(levs)
+        key = (lons.tobytes(), lats.tobytes(), levs.tobytes(), prec)
+        if key == self._grid_key:
+            return
+        capi.check(self.lib.lt_met_grid(self.h, lons.size, lats.size, levs.size,
+                                        capi.ptr(lons), capi.ptr(lats), capi.ptr(levs),
+                                        capi.MET_F64 if prec == "f64" else capi.MET_F32))
+        self._grid_key = key
+        self._slot_keys = [None, None, None]
+
+    def load_met(self, slot: int, met, key=None, close_lon: bool = False) -> None:
+        """Upload a MeteoField-like snapshot into `slot` (copy stream)."""
+        arrs = []
+        src_bytes = 8
+        for name in ("u", "v", "w", "T"):
+            a = np.asarray(getattr(met, name))
+            if a.dtype == np.float32:
+                src_bytes = 4
+            arrs.append(a)
+        dt = np.float32 if src_bytes == 4 else np.float64
+        arrs = [np.ascontiguousarray(a, dtype=dt) for a in arrs]
+        self._met_arrays = arrs  # keep alive until the copy is staged
+        capi.check(self.lib.lt_met_load(self.h, slot, float(met.t_met), src_bytes,
+                                        *[capi.ptr(a) for a in arrs],
+                                        capi.MET_CLOSE_LON if close_lon else 0))
+        self._slot_keys[slot] = key
+
+    def load_met_nodes(self, slot: int, t_met: float, nodes: np.ndarray | int,
+                       close_lon: bool = False, key=None) -> None:
+        """Upload (nx, ny, nz, 4) float32 nodes (numpy array or pinned pointer)."""
+        p = nodes if isinstance(nodes, int) else capi.ptr(nodes)
+        capi.check(self.lib.lt_met_load_nodes(self.h, slot, float(t_met), C.c_void_p(p),
+                                              capi.MET_CLOSE_LON if close_lon else 0))
+        self._slot_keys[slot] = key
+
+    def use_met(self, slot0: int, slot1: int) -> None:
+        capi.check(self.lib.lt_met_use(self.h, slot0, slot1))
+
+    def slot_key(self, slot: int):
+        return self._slot_keys[slot]
+
+    def bind_pair(self, met0, met1) -> None:
+        """Make (met0, met1) the active snapshot pair, uploading only what
+        changed (module-API path; grids must be identical)."""
+        for name in ("lons", "lats", "levs"):
+            if not np.array_equal(np.asarray(getattr(met0, name)), np.asarray(getattr(met1, name))):
+                raise ValueError("met0 and met1 must share one grid on the B200 met store")
+        self.set_grid(met0.lons, met0.lats, met0.levs)
+        k0 = met_fingerprint(met0)
+        k1 = k0 if met1 is met0 else met_fingerprint(met1)
+        slots = {}
+        for key in (k0, k1):
+            if key in slots:
+                continue
+            for s in range(3):
+                if self._slot_keys[s] == key and s not in slots.values():
+                    slots[key] = s
+                    break
+        for key, met in ((k0, met0), (k1, met1)):
+            if key in slots:
+                continue
+            free = next(s for s in range(3) if s not in slots.values())
+            self.load_met(free, met, key)
+            slots[key] = free
+        self.use_met(slots[k0], slots[k1])
+
+    def load_clim(self, clim) -> None:
+        lat, pg = _f64(clim.lat_grid), _f64(clim.p_grid)
+        hno3, pt = _f64(clim.hno3_tab), _f64(clim.p_trop_tab)
+        key = hashlib.blake2b(b"".join(a.tobytes() for a in (lat, pg, hno3, pt))).hexdigest()
+        if key == self._clim_key:
+            return
+        capi.check(self.lib.lt_clim_load(self.h, lat.size, pg.size, capi.ptr(lat), capi.ptr(pg),
+                                         capi.ptr(hno3), capi.ptr(pt)))
+        self._clim_key = key
+
+    # -- compute -----------------------------------------------------------
+    def run(self, ctl, modules: int, start: int, end: int, step: int = 0,
+            faithful_state: int = 0, faithful_base: int = 0, flags: int = 0) -> None:
+        c = ctl if isinstance(ctl, capi.LtControl) else capi.control_struct(ctl)
+        capi.check(self.lib.lt_run(self.h, C.byref(c), modules, start, end, step,
+                                   faithful_state & 0xFFFFFFFFFFFFFFFF, faithful_base, flags))
+
+    def rng_fill(self, mode: int, seed: int, step: int, start: int, end: int) -> None:
+        capi.check(self.lib.lt_rng_fill(self.h, mode, seed & 0xFFFFFFFFFFFFFFFF, step, start, end))
+
+    def iso_counter(self, reset: bool = False) -> int:
+        v = C.c_int64()
+        capi.check(self.lib.lt_iso_counter(self.h, C.byref(v), int(reset)))
+        return int(v.value)
+
+    def sort_by_box(self, start: int, end: int) -> None:
+        capi.check(self.lib.lt_sort_by_box(self.h, start, end))
+
+    def interpolate(self, t, lon, lat, p) -> np.ndarray:
+        lon = _f64(lon)
+        n = lon.size
+        t = _f64(np.broadcast_to(np.asarray(t, dtype=np.float64), (n,)))
+        lat, p = _f64(lat), _f64(p)
+        out = np.empty((4, n))
+        capi.check(self.lib.lt_interpolate(self.h, n, capi.ptr(t), capi.ptr(lon), capi.ptr(lat),
+                                           capi.ptr(p), capi.ptr(out)))
+        return out
+
+    def timing(self, on: bool) -> None:
+        capi.check(self.lib.lt_timing(self.h, int(on)))
+
+    def last_elapsed_ms(self) -> float:
+        v = C.c_float()
+        capi.check(self.lib.lt_last_elapsed_ms(self.h, C.byref(v)))
+        return float(v.value)

@@ -1,0 +1,857 @@
+// lt_capi.cu — the extern "C" boundary (include/lagtrans_b200.h).
+//
+// A context is one GPU's data region: the SoA particle store, up to three
+// met snapshot slots on one grid, the climatology tables, two streams
+// (compute, copy) and the scratch used by the sort and ordered copies.
+// The reference equivalent is one DevicePool worker's ModelImage
+// (device_runtime.py:58-69,165-230).
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/lagtrans_b200.h"
+#include "lt_kernels.cuh"
+
+using namespace lt;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(call)                                                                     \
+  do {                                                                               \
+    cudaError_t e_ = (call);                                                         \
+    if (e_ != cudaSuccess)                                                           \
+      return fail(e_ == cudaErrorMemoryAllocation ? LT_ERR_NOMEM : LT_ERR_CUDA,      \
+                  "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+
+struct AxisHost {
+  double* dev = nullptr;
+  int n = 0;
+  int logscale = 0;
+  float g0 = 0.f, ginv = 0.f;
+};
+
+struct Slot {
+  void* rec = nullptr;  // RecF[] or RecD[]
+  double t_met = 0.0;
+  bool valid = false;
+  cudaEvent_t ready = nullptr;  // recorded on the copy stream after packing
+};
+
+}  // namespace
+
+struct lt_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;  // compute
+  cudaStream_t copy = nullptr;    // met streaming
+  cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
+  cudaEvent_t compute_mark = nullptr;  // last compute-stream work touching met slots
+  bool marked = false;
+  bool timing = false;
+  bool timed_once = false;
+
+  // particles
+  int64_t cap = 0;
+  int32_t nq = 0;
+  double *time = nullptr, *p = nullptr, *zeta = nullptr, *lon = nullptr, *lat = nullptr;
+  double *q = nullptr, *uvwp = nullptr, *iso_var = nullptr, *dt = nullptr;
+  double *rnd_conv = nullptr, *rnd_turb = nullptr, *rnd_meso = nullptr;
+  uint32_t* ids = nullptr;
+  double* scratch = nullptr;     // cap doubles (ordered copies, permutation)
+  uint32_t* sort_buf = nullptr;  // 4 * cap (keys in/out, vals in/out)
+  void* cub_temp = nullptr;
+  size_t cub_bytes = 0;
+  unsigned long long* counters = nullptr;  // [0] iso_nonconverged
+  int* bad = nullptr;
+
+  // met
+  int nx = 0, ny = 0, nz = 0, prec = 0;
+  AxisHost ax_lon, ax_lat, ax_lev;
+  Slot slots[3];
+  int use0 = -1, use1 = -1;
+  void* staging = nullptr;
+  size_t staging_bytes = 0;
+  cudaEvent_t staging_free = nullptr;
+
+  // climatology
+  AxisHost cl_lat, cl_p;
+  double *hno3 = nullptr, *p_trop = nullptr;
+};
+
+namespace {
+
+void free_dev(void* p) {
+  if (p) cudaFree(p);
+}
+
+int alloc_dev(void** p, size_t bytes, const char* what) {
+  cudaError_t e = cudaMalloc(p, bytes ? bytes : 8);
+  if (e != cudaSuccess) {
+    *p = nullptr;
+    return fail(e == cudaErrorMemoryAllocation ? LT_ERR_NOMEM : LT_ERR_CUDA,
+                "cudaMalloc(%s, %zu bytes): %s", what, bytes, cudaGetErrorString(e));
+  }
+  return LT_OK;
+}
+
+// choose the cell-guess mapping of an axis: linear in x, or in log2(x)
+// (geometric pressure levels).  Only speed depends on it, never results.
+int upload_axis(AxisHost& ax, const double* x, int n, cudaStream_t st) {
+  if (n < 2) return fail(LT_ERR_ARG, "axis needs at least 2 nodes, got %d", n);
+  for (int i = 1; i < n; ++i)
+    if (!(x[i] > x[i - 1])) return fail(LT_ERR_ARG, "axis not strictly increasing at %d", i);
+  auto spread = [&](auto f) {
+    const double a = f(x[0]), b = f(x[n - 1]);
+    double worst = 0;
+    for (int i = 0; i < n; ++i) {
+      const double ideal = a + (b - a) * i / (n - 1);
+      worst = fmax(worst, fabs(f(x[i]) - ideal) / ((b - a) / (n - 1)));
+    }
+    return worst;
+  };
+  const double lin = spread([](double v) { return v; });
+  double lg = 1e300;
+  if (x[0] > 0) lg = spread([](double v) { return log2(v); });
+  ax.logscale = lg < lin ? 1 : 0;
+  const double a = ax.logscale ? log2(x[0]) : x[0];
+  const double b = ax.logscale ? log2(x[n - 1]) : x[n - 1];
+  ax.g0 = static_cast<float>(a);
+  ax.ginv = static_cast<float>((n - 1) / (b - a));
+  if (ax.dev && ax.n != n) {
+    cudaFree(ax.dev);
+    ax.dev = nullptr;
+  }
+  ax.n = n;
+  if (!ax.dev) {
+    int rc = alloc_dev(reinterpret_cast<void**>(&ax.dev), sizeof(double) * n, "axis");
+    if (rc) return rc;
+  }
+  CK(cudaMemcpyAsync(ax.dev, x, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+  CK(cudaStreamSynchronize(st));
+  return LT_OK;
+}
+
+Axis view(const AxisHost& a) {
+  Axis v;
+  v.x = a.dev;
+  v.n = a.n;
+  v.logscale = a.logscale;
+  v.g0 = a.g0;
+  v.ginv = a.ginv;
+  return v;
+}
+
+size_t rec_bytes(const lt_ctx* c) { return c->prec == LT_MET_F64 ? sizeof(RecD) : sizeof(RecF); }
+int64_t n_rec(const lt_ctx* c) { return static_cast<int64_t>(c->nx) * c->ny * (c->nz - 1); }
+
+template <class Rec>
+MetView<Rec> met_view(const lt_ctx* c) {
+  MetView<Rec> m;
+  m.lon = view(c->ax_lon);
+  m.lat = view(c->ax_lat);
+  m.lev = view(c->ax_lev);
+  m.ny = c->ny;
+  m.nz = c->nz;
+  m.s0 = static_cast<const Rec*>(c->slots[c->use0].rec);
+  m.s1 = static_cast<const Rec*>(c->slots[c->use1].rec);
+  m.t0 = c->slots[c->use0].t_met;
+  m.t1 = c->slots[c->use1].t_met;
+  return m;
+}
+
+double* field_ptr(lt_ctx* c, int field, int row, int64_t* len, int* rc) {
+  *rc = LT_OK;
+  *len = c->cap;
+  switch (field) {
+    case LT_F_TIME: return c->time;
+    case LT_F_P: return c->p;
+    case LT_F_ZETA: return c->zeta;
+    case LT_F_LON: return c->lon;
+    case LT_F_LAT: return c->lat;
+    case LT_F_Q:
+      if (row < 0 || row >= c->nq) { *rc = fail(LT_ERR_ARG, "q row %d outside [0, %d)", row, c->nq); return nullptr; }
+      return c->q + static_cast<int64_t>(row) * c->cap;
+    case LT_F_UVWP:
+      if (row < 0 || row >= 3) { *rc = fail(LT_ERR_ARG, "uvwp row %d outside [0, 3)", row); return nullptr; }
+      return c->uvwp + static_cast<int64_t>(row) * c->cap;
+    case LT_F_ISO_VAR: return c->iso_var;
+    case LT_F_DT: return c->dt;
+    case LT_F_RND_CONV:
+    case LT_F_RND_TURB:
+    case LT_F_RND_MESO:
+      if (!c->rnd_conv) { *rc = fail(LT_ERR_STATE, "context allocated without a random batch"); return nullptr; }
+      if (field == LT_F_RND_CONV) return c->rnd_conv;
+      *len = 3 * c->cap;
+      return field == LT_F_RND_TURB ? c->rnd_turb : c->rnd_meso;
+    default:
+      *rc = fail(LT_ERR_ARG, "unknown field id %d", field);
+      return nullptr;
+  }
+}
+
+int check_ctx(lt_ctx* c) {
+  if (!c) return fail(LT_ERR_STATE, "null context (deleted region?)");
+  CK(cudaSetDevice(c->device));
+  return LT_OK;
+}
+
+int check_particles(lt_ctx* c) {
+  if (!c->time) return fail(LT_ERR_STATE, "particle store not allocated");
+  return LT_OK;
+}
+
+int ensure_scratch(lt_ctx* c) {
+  if (!c->scratch)
+    return alloc_dev(reinterpret_cast<void**>(&c->scratch), sizeof(double) * c->cap, "scratch");
+  return LT_OK;
+}
+
+int ensure_ids(lt_ctx* c) {
+  if (!c->ids) {
+    int rc = alloc_dev(reinterpret_cast<void**>(&c->ids), sizeof(uint32_t) * c->cap, "ids");
+    if (rc) return rc;
+    CK(launch_iota(c->ids, 0, c->cap, 0, c->stream));
+  }
+  return LT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lt_abi_version(void) { return LT_ABI_VERSION; }
+
+const char* lt_last_error(void) { return g_err.c_str(); }
+
+int lt_device_count(int32_t* n) {
+  int k = 0;
+  cudaError_t e = cudaGetDeviceCount(&k);
+  if (e != cudaSuccess) {
+    *n = 0;
+    return fail(LT_ERR_CUDA, "cudaGetDeviceCount: %s", cudaGetErrorString(e));
+  }
+  *n = k;
+  return LT_OK;
+}
+
+int lt_ctx_create(int32_t device, lt_ctx** out) {
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n)
+    return fail(LT_ERR_ARG, "device_id %d out of range [0, %d)", device, n);
+  CK(cudaSetDevice(device));
+  lt_ctx* c = new lt_ctx();
+  c->device = device;
+  CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+  CK(cudaEventCreate(&c->ev_start));
+  CK(cudaEventCreate(&c->ev_stop));
+  CK(cudaEventCreateWithFlags(&c->staging_free, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->compute_mark, cudaEventDisableTiming));
+  for (auto& s : c->slots) CK(cudaEventCreateWithFlags(&s.ready, cudaEventDisableTiming));
+  int rc = alloc_dev(reinterpret_cast<void**>(&c->counters), 8 * sizeof(unsigned long long), "counters");
+  if (rc) return rc;
+  rc = alloc_dev(reinterpret_cast<void**>(&c->bad), sizeof(int), "flag");
+  if (rc) return rc;
+  CK(cudaMemsetAsync(c->counters, 0, 8 * sizeof(unsigned long long), c->stream));
+  CK(cudaMemsetAsync(c->bad, 0, sizeof(int), c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  *out = c;
+  return LT_OK;
+}
+
+static void free_particles(lt_ctx* c) {
+  for (double** p : {&c->time, &c->p, &c->zeta, &c->lon, &c->lat, &c->q, &c->uvwp, &c->iso_var,
+                     &c->dt, &c->rnd_conv, &c->rnd_turb, &c->rnd_meso, &c->scratch}) {
+    free_dev(*p);
+    *p = nullptr;
+  }
+  free_dev(c->ids); c->ids = nullptr;
+  free_dev(c->sort_buf); c->sort_buf = nullptr;
+  free_dev(c->cub_temp); c->cub_temp = nullptr; c->cub_bytes = 0;
+  c->cap = 0;
+}
+
+int lt_ctx_destroy(lt_ctx* c) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  cudaError_t e1 = cudaStreamSynchronize(c->stream);
+  cudaError_t e2 = cudaStreamSynchronize(c->copy);
+  free_particles(c);
+  for (auto& s : c->slots) {
+    free_dev(s.rec);
+    cudaEventDestroy(s.ready);
+  }
+  free_dev(c->staging);
+  for (AxisHost* a : {&c->ax_lon, &c->ax_lat, &c->ax_lev, &c->cl_lat, &c->cl_p}) free_dev(a->dev);
+  free_dev(c->hno3);
+  free_dev(c->p_trop);
+  free_dev(c->counters);
+  free_dev(c->bad);
+  cudaEventDestroy(c->ev_start);
+  cudaEventDestroy(c->ev_stop);
+  cudaEventDestroy(c->staging_free);
+  cudaEventDestroy(c->compute_mark);
+  cudaStreamDestroy(c->stream);
+  cudaStreamDestroy(c->copy);
+  delete c;
+  if (e1 != cudaSuccess || e2 != cudaSuccess)
+    return fail(LT_ERR_CUDA, "pending work failed before destroy: %s",
+                cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
+  return LT_OK;
+}
+
+int lt_sync(lt_ctx* c) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(c->copy));
+  CK(cudaStreamSynchronize(c->stream));
+  return LT_OK;
+}
+
+int lt_stream(lt_ctx* c, void** s) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  *s = c->stream;
+  return LT_OK;
+}
+
+int lt_particles_alloc(lt_ctx* c, int64_t capacity, int32_t nq, int32_t with_batch) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (capacity < 0) return fail(LT_ERR_ARG, "capacity %lld < 0", (long long)capacity);
+  if (nq < 5) return fail(LT_ERR_ARG, "nq >= 5 violated (meteo sampling needs slots 0..4)");
+  CK(cudaStreamSynchronize(c->stream));
+  free_particles(c);
+  c->cap = capacity;
+  c->nq = nq;
+  const size_t b = sizeof(double) * static_cast<size_t>(capacity);
+  struct { double** p; size_t mult; const char* name; } plan[] = {
+      {&c->time, 1, "time"}, {&c->p, 1, "p"}, {&c->zeta, 1, "zeta"}, {&c->lon, 1, "lon"},
+      {&c->lat, 1, "lat"}, {&c->q, static_cast<size_t>(nq), "q"}, {&c->uvwp, 3, "uvwp"},
+      {&c->iso_var, 1, "iso_var"}, {&c->dt, 1, "dt"}};
+  for (auto& e : plan) {
+    rc = alloc_dev(reinterpret_cast<void**>(e.p), b * e.mult, e.name);
+    if (rc) { free_particles(c); return rc; }
+    CK(cudaMemsetAsync(*e.p, 0, b * e.mult, c->stream));
+  }
+  if (with_batch) {
+    struct { double** p; size_t mult; } bplan[] = {{&c->rnd_conv, 1}, {&c->rnd_turb, 3}, {&c->rnd_meso, 3}};
+    for (auto& e : bplan) {
+      rc = alloc_dev(reinterpret_cast<void**>(e.p), b * e.mult, "random batch");
+      if (rc) { free_particles(c); return rc; }
+      CK(cudaMemsetAsync(*e.p, 0, b * e.mult, c->stream));
+    }
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  return LT_OK;
+}
+
+int lt_field_devptr(lt_ctx* c, int32_t field, int32_t row, void** dev) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if ((rc = check_particles(c))) return rc;
+  if (field == LT_F_ID) {
+    if ((rc = ensure_ids(c))) return rc;
+    *dev = c->ids;
+    return LT_OK;
+  }
+  int64_t len;
+  double* p = field_ptr(c, field, row, &len, &rc);
+  if (rc) return rc;
+  *dev = p;
+  return LT_OK;
+}
+
+static int slice_check(lt_ctx* c, int64_t off, int64_t cnt, int64_t len) {
+  if (off < 0 || cnt < 0 || off + cnt > len)
+    return fail(LT_ERR_RANGE, "range [%lld, %lld) outside field of %lld elements", (long long)off,
+                (long long)(off + cnt), (long long)len);
+  return LT_OK;
+}
+
+int lt_field_h2d(lt_ctx* c, int32_t field, int32_t row, int64_t off, int64_t cnt, const void* host) {
+  int rc = check_ctx(c);
+  if (rc || (rc = check_particles(c))) return rc;
+  if (field == LT_F_ID) {
+    if ((rc = ensure_ids(c)) || (rc = slice_check(c, off, cnt, c->cap))) return rc;
+    if (cnt) CK(cudaMemcpyAsync(c->ids + off, host, 4 * cnt, cudaMemcpyHostToDevice, c->stream));
+    return LT_OK;
+  }
+  int64_t len;
+  double* p = field_ptr(c, field, row, &len, &rc);
+  if (rc || (rc = slice_check(c, off, cnt, len))) return rc;
+  if (cnt) CK(cudaMemcpyAsync(p + off, host, sizeof(double) * cnt, cudaMemcpyHostToDevice, c->stream));
+  return LT_OK;
+}
+
+int lt_field_d2h(lt_ctx* c, int32_t field, int32_t row, int64_t off, int64_t cnt, void* host) {
+  int rc = check_ctx(c);
+  if (rc || (rc = check_particles(c))) return rc;
+  if (field == LT_F_ID) {
+    if ((rc = ensure_ids(c)) || (rc = slice_check(c, off, cnt, c->cap))) return rc;
+    if (cnt) CK(cudaMemcpyAsync(host, c->ids + off, 4 * cnt, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return LT_OK;
+  }
+  int64_t len;
+  double* p = field_ptr(c, field, row, &len, &rc);
+  if (rc || (rc = slice_check(c, off, cnt, len))) return rc;
+  if (cnt) CK(cudaMemcpyAsync(host, p + off, sizeof(double) * cnt, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return LT_OK;
+}
+
+int lt_field_fill(lt_ctx* c, int32_t field, int32_t row, int64_t off, int64_t cnt, double value) {
+  int rc = check_ctx(c);
+  if (rc || (rc = check_particles(c))) return rc;
+  int64_t len;
+  double* p = field_ptr(c, field, row, &len, &rc);
+  if (rc || (rc = slice_check(c, off, cnt, len))) return rc;
+  CK(launch_fill(p + off, cnt, value, c->stream));
+  return LT_OK;
+}
+
+int lt_ids_reset(lt_ctx* c, int64_t off, int64_t cnt, int64_t first_id) {
+  int rc = check_ctx(c);
+  if (rc || (rc = check_particles(c))) return rc;
+  if ((rc = ensure_ids(c)) || (rc = slice_check(c, off, cnt, c->cap))) return rc;
+  if (first_id < 0 || first_id + cnt > (int64_t(1) << 32))
+    return fail(LT_ERR_ARG, "particle ids must fit in 32 bits");
+  CK(launch_iota(c->ids, off, cnt, first_id, c->stream));
+  return LT_OK;
+}
+
+// ------------------------------------------------------------------ met
+
+int lt_met_grid(lt_ctx* c, int32_t nx, int32_t ny, int32_t nz, const double* lons,
+                const double* lats, const double* levs, int32_t precision) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (nx < 2 || ny < 2 || nz < 2) return fail(LT_ERR_ARG, "meteo grid needs nx, ny, nz >= 2");
+  if (precision != LT_MET_F32 && precision != LT_MET_F64)
+    return fail(LT_ERR_ARG, "met precision must be 4 or 8 bytes");
+  std::vector<double> asc(levs, levs + nz);
+  for (int k = 1; k < nz; ++k)
+    if (!(levs[k] < levs[k - 1])) return fail(LT_ERR_ARG, "pressure levels must be strictly decreasing");
+  for (int k = 0; k < nz; ++k) asc[k] = levs[nz - 1 - k];
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaStreamSynchronize(c->copy));
+  if ((rc = upload_axis(c->ax_lon, lons, nx, c->stream))) return rc;
+  if ((rc = upload_axis(c->ax_lat, lats, ny, c->stream))) return rc;
+  if ((rc = upload_axis(c->ax_lev, asc.data(), nz, c->stream))) return rc;
+  const bool same_size = c->nx == nx && c->ny == ny && c->nz == nz && c->prec == precision;
+  c->nx = nx; c->ny = ny; c->nz = nz; c->prec = precision;
+  for (auto& s : c->slots) {
+    s.valid = false;
+    if (!same_size) { free_dev(s.rec); s.rec = nullptr; }
+  }
+  c->use0 = c->use1 = -1;
+  return LT_OK;
+}
+
+static int met_prepare(lt_ctx* c, int slot) {
+  if (!c->nx) return fail(LT_ERR_STATE, "met grid not set");
+  if (slot < 0 || slot > 2) return fail(LT_ERR_ARG, "met slot %d outside [0, 3)", slot);
+  Slot& s = c->slots[slot];
+  // never overwrite a slot the compute stream may still be reading: the copy
+  // stream waits (on the device) for the compute work issued so far
+  if (c->marked) CK(cudaStreamWaitEvent(c->copy, c->compute_mark, 0));
+  if (!s.rec) {
+    int rc = alloc_dev(&s.rec, rec_bytes(c) * n_rec(c), "met slot");
+    if (rc) return rc;
+  }
+  s.valid = false;
+  return LT_OK;
+}
+
+static int ensure_staging(lt_ctx* c, size_t bytes) {
+  if (c->staging_bytes < bytes) {
+    CK(cudaStreamSynchronize(c->copy));
+    free_dev(c->staging);
+    c->staging = nullptr;
+    c->staging_bytes = 0;
+    int rc = alloc_dev(&c->staging, bytes, "met staging");
+    if (rc) return rc;
+    c->staging_bytes = bytes;
+  }
+  return LT_OK;
+}
+
+int lt_met_load(lt_ctx* c, int32_t slot, double t_met, int32_t src_bytes, const void* u,
+                const void* v, const void* w, const void* T, uint32_t flags) {
+  int rc = check_ctx(c);
+  if (rc || (rc = met_prepare(c, slot))) return rc;
+  if (src_bytes != 4 && src_bytes != 8) return fail(LT_ERR_ARG, "met source must be f32 or f64");
+  const int nx_src = (flags & LT_MET_CLOSE_LON) ? c->nx - 1 : c->nx;
+  const size_t fbytes = static_cast<size_t>(nx_src) * c->ny * c->nz * src_bytes;
+  const void* src[4] = {u, v, w, T};
+  if (!(flags & LT_MET_DEVICE_SRC)) {
+    // host fields: stage all four on the device (copy stream), then pack
+    if ((rc = ensure_staging(c, 4 * fbytes))) return rc;
+    char* st = static_cast<char*>(c->staging);
+    for (int f = 0; f < 4; ++f) {
+      CK(cudaMemcpyAsync(st + f * fbytes, src[f], fbytes, cudaMemcpyHostToDevice, c->copy));
+      src[f] = st + f * fbytes;
+    }
+  }
+  Slot& s = c->slots[slot];
+  cudaError_t e;
+  if (src_bytes == 4) {
+    const float* const* b = reinterpret_cast<const float* const*>(src);
+    e = c->prec == LT_MET_F64
+            ? launch_pack_fields<float, RecD>(static_cast<RecD*>(s.rec), b[0], b[1], b[2], b[3], c->nx, c->ny, c->nz, nx_src, c->copy)
+            : launch_pack_fields<float, RecF>(static_cast<RecF*>(s.rec), b[0], b[1], b[2], b[3], c->nx, c->ny, c->nz, nx_src, c->copy);
+  } else {
+    const double* const* b = reinterpret_cast<const double* const*>(src);
+    e = c->prec == LT_MET_F64
+            ? launch_pack_fields<double, RecD>(static_cast<RecD*>(s.rec), b[0], b[1], b[2], b[3], c->nx, c->ny, c->nz, nx_src, c->copy)
+            : launch_pack_fields<double, RecF>(static_cast<RecF*>(s.rec), b[0], b[1], b[2], b[3], c->nx, c->ny, c->nz, nx_src, c->copy);
+  }
+  CK(e);
+  CK(cudaEventRecord(s.ready, c->copy));
+  s.t_met = t_met;
+  s.valid = true;
+  return LT_OK;
+}
+
+int lt_met_load_nodes(lt_ctx* c, int32_t slot, double t_met, const float* uvwT, uint32_t flags) {
+  int rc = check_ctx(c);
+  if (rc || (rc = met_prepare(c, slot))) return rc;
+  const int nx_src = (flags & LT_MET_CLOSE_LON) ? c->nx - 1 : c->nx;
+  const size_t bytes = static_cast<size_t>(nx_src) * c->ny * c->nz * 4 * sizeof(float);
+  const float4* nodes = reinterpret_cast<const float4*>(uvwT);
+  if (!(flags & LT_MET_DEVICE_SRC)) {
+    if ((rc = ensure_staging(c, bytes))) return rc;
+    CK(cudaMemcpyAsync(c->staging, uvwT, bytes, cudaMemcpyHostToDevice, c->copy));
+    nodes = static_cast<const float4*>(c->staging);
+  }
+  Slot& s = c->slots[slot];
+  CK(c->prec == LT_MET_F64
+         ? launch_pack_nodes<RecD>(static_cast<RecD*>(s.rec), nodes, c->nx, c->ny, c->nz, nx_src, c->copy)
+         : launch_pack_nodes<RecF>(static_cast<RecF*>(s.rec), nodes, c->nx, c->ny, c->nz, nx_src, c->copy));
+  CK(cudaEventRecord(s.ready, c->copy));
+  s.t_met = t_met;
+  s.valid = true;
+  return LT_OK;
+}
+
+int lt_met_use(lt_ctx* c, int32_t s0, int32_t s1) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (s0 < 0 || s0 > 2 || s1 < 0 || s1 > 2) return fail(LT_ERR_ARG, "met slots must be in [0, 3)");
+  if (!c->slots[s0].valid || !c->slots[s1].valid) return fail(LT_ERR_STATE, "met slot not loaded");
+  // the compute stream waits for the packing of both snapshots (copy stream)
+  CK(cudaStreamWaitEvent(c->stream, c->slots[s0].ready, 0));
+  CK(cudaStreamWaitEvent(c->stream, c->slots[s1].ready, 0));
+  c->use0 = s0;
+  c->use1 = s1;
+  return LT_OK;
+}
+
+int lt_met_slot_time(lt_ctx* c, int32_t slot, double* t) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (slot < 0 || slot > 2) return fail(LT_ERR_ARG, "met slot outside [0, 3)");
+  if (!c->slots[slot].valid) return fail(LT_ERR_STATE, "met slot %d not loaded", slot);
+  *t = c->slots[slot].t_met;
+  return LT_OK;
+}
+
+int lt_clim_load(lt_ctx* c, int32_t nlat, int32_t np_, const double* lat_grid,
+                 const double* p_grid, const double* hno3, const double* p_trop) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if ((rc = upload_axis(c->cl_lat, lat_grid, nlat, c->stream))) return rc;
+  if ((rc = upload_axis(c->cl_p, p_grid, np_, c->stream))) return rc;
+  free_dev(c->hno3);
+  free_dev(c->p_trop);
+  c->hno3 = c->p_trop = nullptr;
+  if ((rc = alloc_dev(reinterpret_cast<void**>(&c->hno3), sizeof(double) * nlat * np_, "hno3")))
+    return rc;
+  if ((rc = alloc_dev(reinterpret_cast<void**>(&c->p_trop), sizeof(double) * nlat, "p_trop")))
+    return rc;
+  CK(cudaMemcpyAsync(c->hno3, hno3, sizeof(double) * nlat * np_, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->p_trop, p_trop, sizeof(double) * nlat, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return LT_OK;
+}
+
+// ------------------------------------------------------------------ compute
+
+extern "C++" {
+template <class Rec>
+static int run_typed(lt_ctx* c, const lt_control* ctl, uint32_t modules, int64_t start,
+                     int64_t end, int64_t step, uint64_t fstate, int64_t fbase, uint32_t flags) {
+  StepArgs<Rec> a;
+  a.time = c->time; a.p = c->p; a.lon = c->lon; a.lat = c->lat; a.dt = c->dt;
+  a.uvwp = c->uvwp; a.iso_var = c->iso_var; a.q = c->q;
+  a.ids = c->ids;
+  a.rnd_conv = c->rnd_conv; a.rnd_turb = c->rnd_turb; a.rnd_meso = c->rnd_meso;
+  a.cap = c->cap; a.start = start; a.end = end; a.nq = c->nq;
+  a.modules = modules; a.flags = flags; a.step = step;
+  a.faithful_state = fstate; a.faithful_base = fbase;
+  a.iso_nonconv = c->counters;
+  static_assert(sizeof(lt_control) == sizeof(Control), "control layout");
+  std::memcpy(&a.ctl, ctl, sizeof(Control));
+  const bool need_met = modules & (M_ADVECTION | M_TURB | M_MESO | M_SEDI | M_ISOSURF | M_METEO |
+                                   M_ISOSURF_INIT);
+  if (need_met) {
+    if (c->use0 < 0) return fail(LT_ERR_STATE, "no met snapshots selected (lt_met_use)");
+    a.met = met_view<Rec>(c);
+  } else {
+    std::memset(&a.met, 0, sizeof(a.met));
+  }
+  if (modules & M_METEO) {
+    if (!c->hno3) return fail(LT_ERR_STATE, "climatology not loaded (lt_clim_load)");
+    a.clim.lat = view(c->cl_lat);
+    a.clim.p = view(c->cl_p);
+    a.clim.hno3 = c->hno3;
+    a.clim.p_trop = c->p_trop;
+  } else {
+    std::memset(&a.clim, 0, sizeof(a.clim));
+  }
+  CK(launch_step<Rec>(a, c->stream));
+  return LT_OK;
+}
+}  // extern C++
+
+int lt_run(lt_ctx* c, const lt_control* ctl, uint32_t modules, int64_t start, int64_t end,
+           int64_t step, uint64_t fstate, int64_t fbase, uint32_t flags) {
+  int rc = check_ctx(c);
+  if (rc || (rc = check_particles(c))) return rc;
+  if (!(0 <= start && start <= end && end <= c->cap))
+    return fail(LT_ERR_RANGE, "range [%lld, %lld) outside ensemble of %lld particles",
+                (long long)start, (long long)end, (long long)c->cap);
+  if (!(flags & LT_RUN_RNG_INKERNEL) && (modules & (M_TURB | M_MESO | M_CONVECTION)) && !c->rnd_conv)
+    return fail(LT_ERR_STATE, "random batch not allocated and in-kernel draws not requested");
+  if ((flags & LT_RUN_RNG_INKERNEL) && ctl->rng_mode == RNG_FAITHFUL &&
+      (modules & (M_TURB | M_MESO | M_CONVECTION)) && c->ids == nullptr && fbase > start)
+    return fail(LT_ERR_ARG, "faithful base beyond range start");
+  if (c->timing) CK(cudaEventRecord(c->ev_start, c->stream));
+  if (end > start) {
+    rc = c->prec == LT_MET_F64 ? run_typed<RecD>(c, ctl, modules, start, end, step, fstate, fbase, flags)
+                               : run_typed<RecF>(c, ctl, modules, start, end, step, fstate, fbase, flags);
+    if (rc) return rc;
+  }
+  CK(cudaEventRecord(c->compute_mark, c->stream));
+  c->marked = true;
+  if (c->timing) {
+    CK(cudaEventRecord(c->ev_stop, c->stream));
+    c->timed_once = true;
+  }
+  return LT_OK;
+}
+
+int lt_rng_fill(lt_ctx* c, int32_t mode, uint64_t seed, int64_t step, int64_t start, int64_t end) {
+  int rc = check_ctx(c);
+  if (rc || (rc = check_particles(c))) return rc;
+  if (!c->rnd_conv) return fail(LT_ERR_STATE, "context allocated without a random batch");
+  if (!(0 <= start && start <= end && end <= c->cap))
+    return fail(LT_ERR_RANGE, "range [%lld, %lld) outside ensemble of %lld particles",
+                (long long)start, (long long)end, (long long)c->cap);
+  if (mode < 0 || mode > 2) return fail(LT_ERR_ARG, "unknown rng mode %d", mode);
+  if (c->timing) CK(cudaEventRecord(c->ev_start, c->stream));
+  CK(launch_rng_fill(mode, seed, step, start, end, c->rnd_conv, c->rnd_turb, c->rnd_meso, c->stream));
+  if (c->timing) { CK(cudaEventRecord(c->ev_stop, c->stream)); c->timed_once = true; }
+  return LT_OK;
+}
+
+int lt_iso_counter(lt_ctx* c, int64_t* value, int32_t reset) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  unsigned long long v = 0;
+  CK(cudaMemcpyAsync(&v, c->counters, sizeof v, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (reset) {
+    CK(cudaMemsetAsync(c->counters, 0, sizeof v, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  }
+  *value = static_cast<int64_t>(v);
+  return LT_OK;
+}
+
+int lt_interpolate(lt_ctx* c, int64_t n, const double* t, const double* lon, const double* lat,
+                   const double* p, double* out) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (c->use0 < 0) return fail(LT_ERR_STATE, "no met snapshots selected (lt_met_use)");
+  if (n < 0) return fail(LT_ERR_ARG, "negative point count");
+  if (n == 0) return LT_OK;
+  double* buf = nullptr;
+  if ((rc = alloc_dev(reinterpret_cast<void**>(&buf), sizeof(double) * 8 * n, "interp points")))
+    return rc;
+  const double* src[4] = {t, lon, lat, p};
+  cudaError_t e = cudaSuccess;
+  for (int f = 0; f < 4 && e == cudaSuccess; ++f)
+    e = cudaMemcpyAsync(buf + f * n, src[f], sizeof(double) * n, cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess)
+    e = c->prec == LT_MET_F64
+            ? launch_sample<RecD>(met_view<RecD>(c), buf, buf + n, buf + 2 * n, buf + 3 * n, buf + 4 * n, n, c->stream)
+            : launch_sample<RecF>(met_view<RecF>(c), buf, buf + n, buf + 2 * n, buf + 3 * n, buf + 4 * n, n, c->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(out, buf + 4 * n, sizeof(double) * 4 * n, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  cudaFree(buf);
+  CK(e);
+  return LT_OK;
+}
+
+// ------------------------------------------------------------------ sort
+
+extern "C++" {
+template <class Rec>
+static int sort_typed(lt_ctx* c, int64_t start, int64_t end) {
+  const int64_t n = end - start;
+  uint32_t* keys_in = c->sort_buf;
+  uint32_t* keys_out = keys_in + c->cap;
+  uint32_t* vals_in = keys_out + c->cap;
+  uint32_t* vals_out = vals_in + c->cap;
+  const MetView<Rec> m = met_view<Rec>(c);
+  CK(launch_box_keys<Rec>(m, c->lon, c->lat, c->p, start, n, keys_in, vals_in, c->stream));
+  const uint64_t max_key = static_cast<uint64_t>(n_rec(c));
+  int bits = 1;
+  while (bits < 32 && (1ull << bits) <= max_key) ++bits;
+  size_t need = 0;
+  CK(sort_pairs(nullptr, need, keys_in, keys_out, vals_in, vals_out, n, bits, c->stream));
+  if (need > c->cub_bytes) {
+    CK(cudaStreamSynchronize(c->stream));
+    free_dev(c->cub_temp);
+    c->cub_temp = nullptr;
+    int rc = alloc_dev(&c->cub_temp, need, "sort temp");
+    if (rc) return rc;
+    c->cub_bytes = need;
+  }
+  size_t have = c->cub_bytes;
+  CK(sort_pairs(c->cub_temp, have, keys_in, keys_out, vals_in, vals_out, n, bits, c->stream));
+  // permute every per-particle row through the scratch row, swapping pointers
+  std::vector<double**> rows = {&c->time, &c->p, &c->zeta, &c->lon, &c->lat, &c->iso_var, &c->dt};
+  double* scratch = c->scratch;
+  for (double** r : rows) {
+    CK(launch_permute<double>(scratch, *r, vals_out, start, n, c->stream));
+    CK(cudaMemcpyAsync(*r + start, scratch + start, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  for (int k = 0; k < c->nq; ++k) {
+    double* r = c->q + static_cast<int64_t>(k) * c->cap;
+    CK(launch_permute<double>(scratch, r, vals_out, start, n, c->stream));
+    CK(cudaMemcpyAsync(r + start, scratch + start, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  for (int k = 0; k < 3; ++k) {
+    double* r = c->uvwp + static_cast<int64_t>(k) * c->cap;
+    CK(launch_permute<double>(scratch, r, vals_out, start, n, c->stream));
+    CK(cudaMemcpyAsync(r + start, scratch + start, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  CK(launch_permute<uint32_t>(keys_in, c->ids, vals_out, start, n, c->stream));
+  CK(cudaMemcpyAsync(c->ids + start, keys_in + start, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, c->stream));
+  return LT_OK;
+}
+}  // extern C++
+
+int lt_sort_by_box(lt_ctx* c, int64_t start, int64_t end) {
+  int rc = check_ctx(c);
+  if (rc || (rc = check_particles(c))) return rc;
+  if (!(0 <= start && start <= end && end <= c->cap))
+    return fail(LT_ERR_RANGE, "range [%lld, %lld) outside ensemble of %lld particles",
+                (long long)start, (long long)end, (long long)c->cap);
+  if (c->use0 < 0) return fail(LT_ERR_STATE, "no met snapshots selected (lt_met_use)");
+  if (n_rec(c) >= (int64_t(1) << 32)) return fail(LT_ERR_ARG, "met grid too large for 32-bit box keys");
+  if ((rc = ensure_ids(c)) || (rc = ensure_scratch(c))) return rc;
+  if (!c->sort_buf &&
+      (rc = alloc_dev(reinterpret_cast<void**>(&c->sort_buf), 4 * sizeof(uint32_t) * c->cap, "sort keys")))
+    return rc;
+  if (end == start) return LT_OK;
+  if (c->timing) CK(cudaEventRecord(c->ev_start, c->stream));
+  rc = c->prec == LT_MET_F64 ? sort_typed<RecD>(c, start, end) : sort_typed<RecF>(c, start, end);
+  if (rc) return rc;
+  CK(cudaEventRecord(c->compute_mark, c->stream));
+  c->marked = true;
+  if (c->timing) { CK(cudaEventRecord(c->ev_stop, c->stream)); c->timed_once = true; }
+  return LT_OK;
+}
+
+static int ordered_copy(lt_ctx* c, int32_t field, int32_t row, int64_t off, int64_t cnt,
+                        int64_t first_id, void* host, bool to_host) {
+  int rc = check_ctx(c);
+  if (rc || (rc = check_particles(c))) return rc;
+  if (field == LT_F_ID || field == LT_F_RND_CONV || field == LT_F_RND_TURB || field == LT_F_RND_MESO)
+    return fail(LT_ERR_ARG, "ordered copies apply to per-particle state fields only");
+  int64_t len;
+  double* p = field_ptr(c, field, row, &len, &rc);
+  if (rc || (rc = slice_check(c, off, cnt, len))) return rc;
+  if (!c->ids) {  // never sorted: plain copy
+    return to_host ? lt_field_d2h(c, field, row, off, cnt, host)
+                   : lt_field_h2d(c, field, row, off, cnt, host);
+  }
+  if ((rc = ensure_scratch(c))) return rc;
+  if (cnt == 0) return LT_OK;
+  CK(cudaMemsetAsync(c->bad, 0, sizeof(int), c->stream));
+  if (to_host) {
+    CK(launch_unsort(c->scratch, p, c->ids, off, cnt, first_id, c->bad, 1, c->stream));
+    CK(cudaMemcpyAsync(host, c->scratch, sizeof(double) * cnt, cudaMemcpyDeviceToHost, c->stream));
+  } else {
+    CK(cudaMemcpyAsync(c->scratch, host, sizeof(double) * cnt, cudaMemcpyHostToDevice, c->stream));
+    CK(launch_resort(p, c->scratch, c->ids, off, cnt, first_id, c->bad, 1, c->stream));
+  }
+  int bad = 0;
+  CK(cudaMemcpyAsync(&bad, c->bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (bad) return fail(LT_ERR_ARG, "particle ids of [%lld, %lld) are not a permutation of [%lld, %lld)",
+                       (long long)off, (long long)(off + cnt), (long long)first_id,
+                       (long long)(first_id + cnt));
+  return LT_OK;
+}
+
+int lt_field_d2h_ordered(lt_ctx* c, int32_t field, int32_t row, int64_t off, int64_t cnt,
+                         int64_t first_id, void* host) {
+  return ordered_copy(c, field, row, off, cnt, first_id, host, true);
+}
+
+int lt_field_h2d_ordered(lt_ctx* c, int32_t field, int32_t row, int64_t off, int64_t cnt,
+                         int64_t first_id, const void* host) {
+  return ordered_copy(c, field, row, off, cnt, first_id, const_cast<void*>(host), false);
+}
+
+// ------------------------------------------------------------------ timing / host memory
+
+int lt_timing(lt_ctx* c, int32_t enable) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  c->timing = enable != 0;
+  return LT_OK;
+}
+
+int lt_last_elapsed_ms(lt_ctx* c, float* ms) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (!c->timed_once) return fail(LT_ERR_STATE, "no timed launch recorded");
+  CK(cudaEventSynchronize(c->ev_stop));
+  CK(cudaEventElapsedTime(ms, c->ev_start, c->ev_stop));
+  return LT_OK;
+}
+
+int lt_host_alloc(int64_t bytes, void** out) {
+  CK(cudaHostAlloc(out, static_cast<size_t>(bytes), cudaHostAllocPortable));
+  return LT_OK;
+}
+
+int lt_host_free(void* p) {
+  CK(cudaFreeHost(p));
+  return LT_OK;
+}
+
+}  // extern "C"

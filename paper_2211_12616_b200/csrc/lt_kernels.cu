@@ -1,0 +1,232 @@
+// lt_kernels.cu — kernels other than the step: met packing, random-batch
+// fill, box keys for the sort, SoA permutation and ordered copies.
+#include "lt_kernels.cuh"
+
+namespace lt {
+
+// Pack (nx_src, ny, nz) field arrays into node-pair records (u,v,w,T at k
+// and k+1 per (i,j,k), k < nz-1).  With close_lon the destination has one
+// more longitude column, a copy of column 0 (ingest.py:195-207).
+template <class Src, class Rec>
+__global__ void pack_fields_kernel(Rec* out, const Src* u, const Src* v, const Src* w,
+                                   const Src* T, int nx, int ny, int nz, int nx_src) {
+  const int64_t nrec = static_cast<int64_t>(nx) * ny * (nz - 1);
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < nrec;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int k = static_cast<int>(r % (nz - 1));
+    const int64_t col = r / (nz - 1);
+    const int j = static_cast<int>(col % ny);
+    int i = static_cast<int>(col / ny);
+    if (i >= nx_src) i -= nx_src;
+    const int64_t b = (static_cast<int64_t>(i) * ny + j) * nz + k;
+    Rec rec;
+    store_node(rec, 0, u[b], v[b], w[b], T[b]);
+    store_node(rec, 1, u[b + 1], v[b + 1], w[b + 1], T[b + 1]);
+    out[r] = rec;
+  }
+}
+
+template <class Rec>
+__global__ void pack_nodes_kernel(Rec* out, const float4* nodes, int nx, int ny, int nz,
+                                  int nx_src) {
+  const int64_t nrec = static_cast<int64_t>(nx) * ny * (nz - 1);
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < nrec;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int k = static_cast<int>(r % (nz - 1));
+    const int64_t col = r / (nz - 1);
+    const int j = static_cast<int>(col % ny);
+    int i = static_cast<int>(col / ny);
+    if (i >= nx_src) i -= nx_src;
+    const int64_t b = (static_cast<int64_t>(i) * ny + j) * nz + k;
+    const float4 n0 = nodes[b], n1 = nodes[b + 1];
+    Rec rec;
+    store_node(rec, 0, n0.x, n0.y, n0.z, n0.w);
+    store_node(rec, 1, n1.x, n1.y, n1.z, n1.w);
+    out[r] = rec;
+  }
+}
+
+// rng.py:156-181: fill the RandomBatch of [start, end)
+__global__ void rng_fill_kernel(int mode, uint64_t seed_or_state, int64_t step, int64_t start,
+                                int64_t end, double* conv, double* turb, double* meso) {
+  for (int64_t s = start + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < end;
+       s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double c, t[3], m[3];
+    if (mode == RNG_COUNTER) {
+      c = to_unit(counter_word(seed_or_state, step, static_cast<uint64_t>(s), 0, 0));
+      counter_normals(seed_or_state, step, static_cast<uint64_t>(s), 1, t);
+      counter_normals(seed_or_state, step, static_cast<uint64_t>(s), 2, m);
+    } else if (mode == RNG_FAITHFUL) {
+      faithful_draws(seed_or_state, static_cast<uint64_t>(s - start), c, t, m);
+    } else {
+      philox_draws(seed_or_state, step, static_cast<uint64_t>(s), c, t, m);
+    }
+    conv[s] = c;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      turb[3 * s + k] = t[k];
+      meso[3 * s + k] = m[k];
+    }
+  }
+}
+
+template <class Rec>
+__global__ void box_key_kernel(MetView<Rec> m, const double* lon, const double* lat,
+                               const double* p, int64_t start, int64_t n, uint32_t* keys,
+                               uint32_t* vals) {
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t s = start + t;
+    const Cell c = cell_of(m, lon[s], lat[s], p[s]);
+    keys[t] = static_cast<uint32_t>(c.r00);
+    vals[t] = static_cast<uint32_t>(t);
+  }
+}
+
+template <class T>
+__global__ void permute_kernel(T* dst, const T* src, const uint32_t* perm, int64_t start,
+                               int64_t n) {
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[start + t] = src[start + perm[t]];
+}
+
+// scatter a sorted slice into original order: out[id - first] = in[s]
+template <class T>
+__global__ void unsort_kernel(T* out, const T* in, const uint32_t* ids, int64_t offset,
+                              int64_t count, int64_t first_id, int* bad, int stride_in) {
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < count;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t dst = static_cast<int64_t>(ids[offset + t]) - first_id;
+    if (dst < 0 || dst >= count) { *bad = 1; continue; }
+    for (int c = 0; c < stride_in; ++c) out[dst * stride_in + c] = in[(offset + t) * stride_in + c];
+  }
+}
+
+// gather original order into the sorted slice: out[s] = in[id - first]
+template <class T>
+__global__ void resort_kernel(T* out, const T* in, const uint32_t* ids, int64_t offset,
+                              int64_t count, int64_t first_id, int* bad, int stride_in) {
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < count;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t src = static_cast<int64_t>(ids[offset + t]) - first_id;
+    if (src < 0 || src >= count) { *bad = 1; continue; }
+    for (int c = 0; c < stride_in; ++c) out[(offset + t) * stride_in + c] = in[src * stride_in + c];
+  }
+}
+
+// physics.py:69-79 as a standalone call (interpolate_met at arbitrary points)
+template <class Rec>
+__global__ void sample_kernel(MetView<Rec> m, const double* t, const double* lon, const double* lat,
+                              const double* p, double* out, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double v[4];
+    sample(m, t[i], lon[i], lat[i], p[i], 15, v);
+#pragma unroll
+    for (int f = 0; f < 4; ++f) out[f * n + i] = v[f];
+  }
+}
+
+__global__ void iota_kernel(uint32_t* ids, int64_t offset, int64_t count, int64_t first) {
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < count;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    ids[offset + t] = static_cast<uint32_t>(first + t);
+}
+
+__global__ void fill_kernel(double* x, int64_t n, double v) {
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    x[t] = v;
+}
+
+// ---------------------------------------------------------------- launchers
+
+static int grid_for(int64_t n, int block = 256) {
+  int64_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > 148 * 64) g = 148 * 64;
+  return static_cast<int>(g);
+}
+
+template <class Src, class Rec>
+cudaError_t launch_pack_fields(Rec* out, const Src* u, const Src* v, const Src* w, const Src* T,
+                               int nx, int ny, int nz, int nx_src, cudaStream_t st) {
+  const int64_t n = static_cast<int64_t>(nx) * ny * (nz - 1);
+  pack_fields_kernel<Src, Rec><<<grid_for(n), 256, 0, st>>>(out, u, v, w, T, nx, ny, nz, nx_src);
+  return cudaGetLastError();
+}
+template cudaError_t launch_pack_fields<float, RecF>(RecF*, const float*, const float*, const float*, const float*, int, int, int, int, cudaStream_t);
+template cudaError_t launch_pack_fields<double, RecF>(RecF*, const double*, const double*, const double*, const double*, int, int, int, int, cudaStream_t);
+template cudaError_t launch_pack_fields<float, RecD>(RecD*, const float*, const float*, const float*, const float*, int, int, int, int, cudaStream_t);
+template cudaError_t launch_pack_fields<double, RecD>(RecD*, const double*, const double*, const double*, const double*, int, int, int, int, cudaStream_t);
+
+template <class Rec>
+cudaError_t launch_pack_nodes(Rec* out, const float4* nodes, int nx, int ny, int nz, int nx_src,
+                              cudaStream_t st) {
+  const int64_t n = static_cast<int64_t>(nx) * ny * (nz - 1);
+  pack_nodes_kernel<Rec><<<grid_for(n), 256, 0, st>>>(out, nodes, nx, ny, nz, nx_src);
+  return cudaGetLastError();
+}
+template cudaError_t launch_pack_nodes<RecF>(RecF*, const float4*, int, int, int, int, cudaStream_t);
+template cudaError_t launch_pack_nodes<RecD>(RecD*, const float4*, int, int, int, int, cudaStream_t);
+
+cudaError_t launch_rng_fill(int mode, uint64_t seed, int64_t step, int64_t start, int64_t end,
+                            double* conv, double* turb, double* meso, cudaStream_t st) {
+  if (end <= start) return cudaSuccess;
+  rng_fill_kernel<<<grid_for(end - start), 256, 0, st>>>(mode, seed, step, start, end, conv, turb, meso);
+  return cudaGetLastError();
+}
+
+template <class Rec>
+cudaError_t launch_box_keys(const MetView<Rec>& m, const double* lon, const double* lat,
+                            const double* p, int64_t start, int64_t n, uint32_t* keys,
+                            uint32_t* vals, cudaStream_t st) {
+  box_key_kernel<Rec><<<grid_for(n), 256, 0, st>>>(m, lon, lat, p, start, n, keys, vals);
+  return cudaGetLastError();
+}
+template cudaError_t launch_box_keys<RecF>(const MetView<RecF>&, const double*, const double*, const double*, int64_t, int64_t, uint32_t*, uint32_t*, cudaStream_t);
+template cudaError_t launch_box_keys<RecD>(const MetView<RecD>&, const double*, const double*, const double*, int64_t, int64_t, uint32_t*, uint32_t*, cudaStream_t);
+
+template <class T>
+cudaError_t launch_permute(T* dst, const T* src, const uint32_t* perm, int64_t start, int64_t n,
+                           cudaStream_t st) {
+  permute_kernel<T><<<grid_for(n), 256, 0, st>>>(dst, src, perm, start, n);
+  return cudaGetLastError();
+}
+template cudaError_t launch_permute<double>(double*, const double*, const uint32_t*, int64_t, int64_t, cudaStream_t);
+template cudaError_t launch_permute<uint32_t>(uint32_t*, const uint32_t*, const uint32_t*, int64_t, int64_t, cudaStream_t);
+
+cudaError_t launch_unsort(double* out, const double* in, const uint32_t* ids, int64_t offset,
+                          int64_t count, int64_t first_id, int* bad, int stride, cudaStream_t st) {
+  unsort_kernel<double><<<grid_for(count), 256, 0, st>>>(out, in, ids, offset, count, first_id, bad, stride);
+  return cudaGetLastError();
+}
+cudaError_t launch_resort(double* out, const double* in, const uint32_t* ids, int64_t offset,
+                          int64_t count, int64_t first_id, int* bad, int stride, cudaStream_t st) {
+  resort_kernel<double><<<grid_for(count), 256, 0, st>>>(out, in, ids, offset, count, first_id, bad, stride);
+  return cudaGetLastError();
+}
+template <class Rec>
+cudaError_t launch_sample(const MetView<Rec>& m, const double* t, const double* lon,
+                          const double* lat, const double* p, double* out, int64_t n,
+                          cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  sample_kernel<Rec><<<grid_for(n), 256, 0, st>>>(m, t, lon, lat, p, out, n);
+  return cudaGetLastError();
+}
+template cudaError_t launch_sample<RecF>(const MetView<RecF>&, const double*, const double*, const double*, const double*, double*, int64_t, cudaStream_t);
+template cudaError_t launch_sample<RecD>(const MetView<RecD>&, const double*, const double*, const double*, const double*, double*, int64_t, cudaStream_t);
+
+cudaError_t launch_iota(uint32_t* ids, int64_t offset, int64_t count, int64_t first, cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  iota_kernel<<<grid_for(count), 256, 0, st>>>(ids, offset, count, first);
+  return cudaGetLastError();
+}
+cudaError_t launch_fill(double* x, int64_t n, double v, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  fill_kernel<<<grid_for(n), 256, 0, st>>>(x, n, v);
+  return cudaGetLastError();
+}
+
+}  // namespace lt

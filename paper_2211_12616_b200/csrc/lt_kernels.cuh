@@ -1,0 +1,54 @@
+// lt_kernels.cuh — launcher declarations shared by the kernels and the C ABI.
+#pragma once
+
+#include "lt_step.cuh"
+
+namespace lt {
+
+__device__ __forceinline__ void store_node(RecF& r, int which, double u, double v, double w,
+                                           double T) {
+  float* d = which ? r.b : r.a;
+  d[0] = static_cast<float>(u); d[1] = static_cast<float>(v);
+  d[2] = static_cast<float>(w); d[3] = static_cast<float>(T);
+}
+__device__ __forceinline__ void store_node(RecD& r, int which, double u, double v, double w,
+                                           double T) {
+  double* d = which ? r.b.v : r.a.v;
+  d[0] = u; d[1] = v; d[2] = w; d[3] = T;
+}
+
+template <class Src, class Rec>
+cudaError_t launch_pack_fields(Rec* out, const Src* u, const Src* v, const Src* w, const Src* T,
+                               int nx, int ny, int nz, int nx_src, cudaStream_t st);
+template <class Rec>
+cudaError_t launch_pack_nodes(Rec* out, const float4* nodes, int nx, int ny, int nz, int nx_src,
+                              cudaStream_t st);
+cudaError_t launch_rng_fill(int mode, uint64_t seed, int64_t step, int64_t start, int64_t end,
+                            double* conv, double* turb, double* meso, cudaStream_t st);
+template <class Rec>
+cudaError_t launch_box_keys(const MetView<Rec>& m, const double* lon, const double* lat,
+                            const double* p, int64_t start, int64_t n, uint32_t* keys,
+                            uint32_t* vals, cudaStream_t st);
+template <class T>
+cudaError_t launch_permute(T* dst, const T* src, const uint32_t* perm, int64_t start, int64_t n,
+                           cudaStream_t st);
+cudaError_t launch_unsort(double* out, const double* in, const uint32_t* ids, int64_t offset,
+                          int64_t count, int64_t first_id, int* bad, int stride, cudaStream_t st);
+cudaError_t launch_resort(double* out, const double* in, const uint32_t* ids, int64_t offset,
+                          int64_t count, int64_t first_id, int* bad, int stride, cudaStream_t st);
+template <class Rec>
+cudaError_t launch_sample(const MetView<Rec>& m, const double* t, const double* lon,
+                          const double* lat, const double* p, double* out, int64_t n,
+                          cudaStream_t st);
+cudaError_t launch_iota(uint32_t* ids, int64_t offset, int64_t count, int64_t first,
+                        cudaStream_t st);
+cudaError_t launch_fill(double* x, int64_t n, double v, cudaStream_t st);
+
+template <class Rec>
+cudaError_t launch_step(const StepArgs<Rec>& a, cudaStream_t st);
+
+cudaError_t sort_pairs(void* temp, size_t& temp_bytes, const uint32_t* keys_in,
+                       uint32_t* keys_out, const uint32_t* vals_in, uint32_t* vals_out,
+                       int64_t n, int end_bit, cudaStream_t st);
+
+}  // namespace lt

@@ -1,0 +1,48 @@
+// lt_step.cu — launch of the fused step kernel (+ CUB sort wrapper).
+#include <cub/cub.cuh>
+
+#include "lt_kernels.cuh"
+
+namespace lt {
+
+// module sets compiled as their own specialisation (dead modules removed)
+constexpr uint32_t kChainAdv = M_TIMESTEPS | M_ADVECTION | M_POSITION;
+constexpr uint32_t kChainAdvDiff = M_TIMESTEPS | M_ADVECTION | M_TURB | M_MESO | M_POSITION;
+
+template <class Rec, uint32_t FIXED>
+static cudaError_t launch_fixed(const StepArgs<Rec>& a, cudaStream_t st) {
+  static int blocks_per_sm = 0;
+  static int sms = 0;
+  if (!blocks_per_sm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, step_kernel<Rec, FIXED>, 256, 0);
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+  }
+  const int64_t n = a.end - a.start;
+  if (n <= 0) return cudaSuccess;
+  int64_t grid = (n + 255) / 256;
+  const int64_t cap = static_cast<int64_t>(sms) * blocks_per_sm * 16;
+  if (grid > cap) grid = cap;
+  step_kernel<Rec, FIXED><<<static_cast<unsigned>(grid), 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <class Rec>
+cudaError_t launch_step(const StepArgs<Rec>& a, cudaStream_t st) {
+  if (a.modules == kChainAdvDiff) return launch_fixed<Rec, kChainAdvDiff>(a, st);
+  if (a.modules == kChainAdv) return launch_fixed<Rec, kChainAdv>(a, st);
+  return launch_fixed<Rec, 0>(a, st);
+}
+template cudaError_t launch_step<RecF>(const StepArgs<RecF>&, cudaStream_t);
+template cudaError_t launch_step<RecD>(const StepArgs<RecD>&, cudaStream_t);
+
+cudaError_t sort_pairs(void* temp, size_t& temp_bytes, const uint32_t* keys_in,
+                       uint32_t* keys_out, const uint32_t* vals_in, uint32_t* vals_out,
+                       int64_t n, int end_bit, cudaStream_t st) {
+  return cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, vals_in, vals_out,
+                                         static_cast<int>(n), 0, end_bit, st);
+}
+
+}  // namespace lt

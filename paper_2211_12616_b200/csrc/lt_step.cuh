@@ -1,0 +1,241 @@
+// lt_step.cuh — the fused per-particle time step kernel.
+//
+// One thread advances one particle through the enabled modules in the
+// reference pipeline order (driver_cli.py:31-33, :151-183):
+//   timesteps -> [random draws] -> advection -> turb -> meso -> convection
+//   -> sedi -> decay -> isosurf -> position -> meteo
+// Particle state lives in registers between modules, so a fused step reads
+// and writes each SoA field once.  Per-module calls from the drop-in module
+// API launch the same kernel with a single module bit.
+#pragma once
+
+#include "lt_device.cuh"
+
+namespace lt {
+
+template <class Rec>
+struct StepArgs {
+  // particle store (SoA, row stride `cap` for q and uvwp)
+  double* time;
+  double* p;
+  double* lon;
+  double* lat;
+  double* dt;
+  double* uvwp;
+  double* iso_var;
+  double* q;
+  const uint32_t* ids;  // global particle index per slot, or null (= slot)
+  const double* rnd_conv;
+  const double* rnd_turb;
+  const double* rnd_meso;
+  int64_t cap, start, end;
+  int32_t nq;
+  uint32_t modules, flags;
+  int64_t step;
+  uint64_t faithful_state;
+  int64_t faithful_base;
+  unsigned long long* iso_nonconv;
+  Control ctl;
+  MetView<Rec> met;
+  Clim clim;
+};
+
+template <class Rec, uint32_t FIXED>
+__global__ void __launch_bounds__(256) step_kernel(const StepArgs<Rec> a) {
+  const uint32_t mods = FIXED ? FIXED : a.modules;
+  const Control& ctl = a.ctl;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  unsigned long long nonconv = 0;
+
+  for (int64_t s = a.start + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+       s < a.end; s += stride) {
+    double time = a.time[s], lon = a.lon[s], lat = a.lat[s], p = a.p[s];
+
+    // physics.py:82-88 (module_timesteps)
+    double dt;
+    if ((mods & M_TIMESTEPS) || !(a.flags & F_DT_ARRAY)) {
+      dt = fmin(ctl.dt_model, ctl.t_stop - time);
+      dt = fmin(fmax(dt, 0.0), ctl.dt_model);
+      if ((mods & M_TIMESTEPS) && (a.flags & F_WRITE_DT)) a.dt[s] = dt;
+    } else {
+      dt = a.dt[s];
+    }
+    const bool act = dt > 0.0;
+
+    // random draws: rng.py:156-181 (in-kernel) or the caller's RandomBatch
+    const bool want_turb = (mods & M_TURB) && (ctl.turb_dx != 0.0 || ctl.turb_dz != 0.0);
+    const bool want_meso = (mods & M_MESO) && ctl.turb_meso != 0.0;
+    const bool want_conv = (mods & M_CONVECTION) && ctl.conv_prob != 0.0;
+    double xc = 0.0, xt[3] = {0.0, 0.0, 0.0}, xm[3] = {0.0, 0.0, 0.0};
+    if (want_turb || want_meso || want_conv) {
+      if (a.flags & F_RNG_INKERNEL) {
+        const uint64_t gid = a.ids ? static_cast<uint64_t>(a.ids[s]) : static_cast<uint64_t>(s);
+        if (ctl.rng_mode == RNG_COUNTER) {
+          const uint64_t seed = ctl.rng_seed_global;
+          if (want_conv) xc = to_unit(counter_word(seed, a.step, gid, 0, 0));
+          if (want_turb) counter_normals(seed, a.step, gid, 1, xt);
+          if (want_meso) counter_normals(seed, a.step, gid, 2, xm);
+        } else if (ctl.rng_mode == RNG_FAITHFUL) {
+          faithful_draws(a.faithful_state, gid - static_cast<uint64_t>(a.faithful_base), xc, xt, xm);
+        } else {
+          philox_draws(ctl.rng_seed_global, a.step, gid, xc, xt, xm);
+        }
+      } else {
+        if (want_conv) xc = a.rnd_conv[s];
+        if (want_turb) { xt[0] = a.rnd_turb[3 * s]; xt[1] = a.rnd_turb[3 * s + 1]; xt[2] = a.rnd_turb[3 * s + 2]; }
+        if (want_meso) { xm[0] = a.rnd_meso[3 * s]; xm[1] = a.rnd_meso[3 * s + 1]; xm[2] = a.rnd_meso[3 * s + 2]; }
+      }
+    }
+
+    // physics.py:225-235 (module_isosurf_init)
+    if ((mods & M_ISOSURF_INIT) && ctl.isosurf_mode != ISO_OFF) {
+      if (ctl.isosurf_mode == ISO_PRESSURE) {
+        a.iso_var[s] = p;
+      } else {
+        double v[4];
+        sample(a.met, time, lon, lat, p, 8, v);
+        a.iso_var[s] = v[3] * pow(1000.0 / p, kKappa);
+      }
+    }
+
+    // physics.py:91-116 (module_advection): explicit midpoint
+    if ((mods & M_ADVECTION) && act) {
+      double w0[4], w1[4];
+      sample(a.met, time, lon, lat, p, 7, w0);
+      const double half = 0.5 * dt;
+      const double lon_m = lon + w0[0] * half * kDegPerM / cos_lat(lat);
+      const double lat_m = lat + w0[1] * half * kDegPerM;
+      const double p_m = p + w0[2] * half;
+      sample(a.met, time + half, lon_m, lat_m, p_m, 7, w1);
+      lon = lon + w1[0] * dt * kDegPerM / cos_lat(lat_m);
+      lat = lat + w1[1] * dt * kDegPerM;
+      p = p + w1[2] * dt;
+      time = time + dt;
+    }
+
+    // physics.py:119-147 (module_diffusion_turb); the vertical part sees the
+    // post-hop lon/lat and pre-hop p (numpy view aliasing)
+    if (want_turb && act) {
+      if (ctl.turb_dx > 0.0) {
+        const double sig = sqrt(2.0 * ctl.turb_dx * dt);
+        const double nlon = lon + sig * xt[0] * kDegPerM / cos_lat(lat);
+        lat = lat + sig * xt[1] * kDegPerM;
+        lon = nlon;
+      }
+      if (ctl.turb_dz > 0.0) {
+        double v[4];
+        sample(a.met, time, lon, lat, p, 8, v);
+        const double dz = sqrt(2.0 * ctl.turb_dz * dt) * xt[2];
+        const double rho = 100.0 * p / (kRAir * v[3]);
+        p = p + (-(rho * kG0 * dz) / 100.0);
+      }
+    }
+
+    // physics.py:150-188 (module_diffusion_meso): AR(1) with met0 cell spread
+    if (want_meso && act) {
+      const Cell c = cell_of(a.met, lon, lat, p);
+      Corners<Rec> q;
+      gather(a.met.s0, a.met, c.r00, q);
+      double r = 1.0 - 2.0 * dt / ctl.met_dt;
+      r = fmin(fmax(r, 0.0), 1.0);
+      const double amp = sqrt(1.0 - r * r);
+      double pert[3];
+#pragma unroll
+      for (int f = 0; f < 3; ++f) {
+        const double sigma = ctl.turb_meso * corner_std(q, f);
+        pert[f] = r * a.uvwp[f * a.cap + s] + amp * sigma * xm[f];
+        a.uvwp[f * a.cap + s] = pert[f];
+      }
+      const double nlon = lon + pert[0] * dt * kDegPerM / cos_lat(lat);
+      lat = lat + pert[1] * dt * kDegPerM;
+      lon = nlon;
+      p = p + pert[2] * dt;
+    }
+
+    // physics.py:191-203 (module_convection)
+    if (want_conv && act && p > ctl.conv_p_top && xc < ctl.conv_prob)
+      p = ctl.conv_p_top + (xc / ctl.conv_prob) * (ctl.p_surf - ctl.conv_p_top);
+
+    // physics.py:206-222 (module_sedi): Stokes settling
+    if ((mods & M_SEDI) && ctl.sedi_radius != 0.0 && act) {
+      double v[4];
+      sample(a.met, time, lon, lat, p, 8, v);
+      const double rho = 100.0 * p / (kRAir * v[3]);
+      const double vs = 2.0 * (ctl.sedi_radius * ctl.sedi_radius) * (ctl.sedi_density - rho) *
+                        kG0 / (9.0 * kEtaAir);
+      p = p + (rho * kG0 * vs * dt) / 100.0;
+    }
+
+    // decay (new module): q[slot] *= exp(-dt / tau) while active
+    if ((mods & M_DECAY) && ctl.decay_tau > 0.0 && act && ctl.decay_slot >= 0 &&
+        ctl.decay_slot < a.nq) {
+      double* qs = a.q + static_cast<int64_t>(ctl.decay_slot) * a.cap + s;
+      *qs = *qs * exp(-dt / ctl.decay_tau);
+    }
+
+    // physics.py:238-264 (module_isosurf): applies to every particle
+    if ((mods & M_ISOSURF) && ctl.isosurf_mode != ISO_OFF) {
+      if (ctl.isosurf_mode == ISO_PRESSURE) {
+        p = a.iso_var[s];
+      } else {
+        const double theta0 = a.iso_var[s];
+        bool pending = true;
+        for (int it = 0; it < 10 && pending; ++it) {
+          double v[4];
+          sample(a.met, time, lon, lat, p, 8, v);
+          const double pn = 1000.0 * pow(v[3] / theta0, kInvKappa);
+          const double dp = pn - p;
+          p = pn;
+          pending = fabs(dp) >= 0.1;
+        }
+        nonconv += pending ? 1ull : 0ull;
+      }
+    }
+
+    // physics.py:267-287 (module_position): pole reflection, lon wrap, clamp
+    if (mods & M_POSITION) {
+      while (fabs(lat) > 90.0) {
+        lat = (lat > 0.0 ? 1.0 : -1.0) * (180.0 - fabs(lat));
+        lon = lon + 180.0;
+      }
+      if (lon < -180.0 || lon >= 180.0) {
+        double m = fmod(lon + 180.0, 360.0);  // np.mod: result takes the divisor's sign
+        if (m != 0.0) {
+          if (m < 0.0) m += 360.0;
+        } else {
+          m = 0.0;
+        }
+        lon = m - 180.0;
+      }
+      p = fmin(fmax(p, ctl.p_top), ctl.p_surf);
+    }
+
+    // physics.py:290-301 (module_meteo): sample T,u,v and climatology
+    if (mods & M_METEO) {
+      double v[4];
+      sample(a.met, time, lon, lat, p, 11, v);
+      a.q[s] = v[3];
+      a.q[a.cap + s] = v[0];
+      a.q[2 * a.cap + s] = v[1];
+      a.q[3 * a.cap + s] = clim_hno3(a.clim, lat, p);
+      a.q[4 * a.cap + s] = p < clim_ptrop(a.clim, lat) ? 1.0 : 0.0;
+    }
+
+    if (mods & (M_ADVECTION | M_TURB | M_MESO | M_CONVECTION | M_SEDI | M_ISOSURF | M_POSITION)) {
+      a.p[s] = p;
+      a.lon[s] = lon;
+      a.lat[s] = lat;
+      if (mods & M_ADVECTION) a.time[s] = time;
+    }
+  }
+
+  if (mods & M_ISOSURF) {
+    // warp-aggregated counter (CacheState.iso_nonconverged)
+    unsigned long long tot = nonconv;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_down_sync(0xffffffffu, tot, o);
+    if ((threadIdx.x & 31) == 0 && tot) atomicAdd(a.iso_nonconv, tot);
+  }
+}
+
+}  // namespace lt

@@ -1,0 +1,161 @@
+"""GPU: the fused device-resident engine (one launch per step, in-kernel
+random draws, box sort, met rotation) against the reference's golden runs,
+the oracle and the module-by-module path."""
+
+import numpy as np
+import pytest
+
+from conftest import chain_ctl, control, snapshot_from
+from oracle import lagtrans_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def eng():
+    from paper_2211_12616_b200 import engine, model_state, synthetic
+    return engine, model_state, synthetic
+
+
+def _ens(ms, g, tag):
+    return ms.ParticleEnsemble(np=g[f"{tag}_p"].size, time=g[f"{tag}_time"].copy(),
+                               p=g[f"{tag}_p"].copy(), zeta=g[f"{tag}_zeta"].copy(),
+                               lon=g[f"{tag}_lon"].copy(), lat=g[f"{tag}_lat"].copy(),
+                               q=g[f"{tag}_q"].copy())
+
+
+def _run_chain(engine, ms, g, ctl, steps, shards=1, sort_every=0):
+    m0, m1 = snapshot_from(g, "m0"), snapshot_from(g, "m1")
+    from paper_2211_12616_b200.partition import partition_all
+    ens = _ens(ms, g, "init")
+    cache = ms.cache_allocate(ens.np)
+    mask = engine.FULL
+    for w in partition_all(ens.np, shards):
+        e = engine.Engine(device=0, first_id=w.start)
+        e.upload(ens, start=w.start, end=w.end)
+        e.bind_met(m0, m1)
+        e.load_clim(ms.read_clim(ctl))
+        e.init_isosurf(ctl)
+        for step in range(steps):
+            if sort_every and step % sort_every == 0:
+                e.sort()
+            e.step(ctl, step, mask, device_id=w.device_id)
+        e.download(ens, cache, start=w.start)
+        e.close()
+    return ens, cache
+
+
+def test_fused_chain_matches_reference_golden(eng, golden_chain):
+    engine, ms, _ = eng
+    g = golden_chain
+    ens, cache = _run_chain(engine, ms, g, chain_ctl(), 50, shards=2)
+    np.testing.assert_array_equal(ens.time, g["final_time"])
+    for k in ("lon", "lat", "p"):
+        np.testing.assert_allclose(getattr(ens, k), g[f"final_{k}"], rtol=1e-9, atol=1e-9)
+
+
+def test_fused_equals_module_by_module_bitwise(eng, golden_chain):
+    """Counter mode: in-kernel draws == generate_random_nums batch, so the
+    fused launch reproduces the eight-module pipeline bit for bit."""
+    engine, ms, _ = eng
+    from test_gpu_parity import _module_chain
+    import paper_2211_12616_b200.physics as phys
+    import paper_2211_12616_b200.rng as rng
+    g = golden_chain
+    ctl = chain_ctl()
+    fused, _ = _run_chain(engine, ms, g, ctl, 12, shards=1)
+    mod, _ = _module_chain(phys, rng, ms, ctl, g, snapshot_from(g, "m0"),
+                           snapshot_from(g, "m1"), 12, parts=1)
+    for k in ("lon", "lat", "p", "time"):
+        np.testing.assert_array_equal(getattr(fused, k), getattr(mod, k))
+
+
+def test_shard_count_invariance(eng, golden_chain):
+    """Acceptance c1 on the GPU engine: 1, 2, 3 shards are byte-identical."""
+    engine, ms, _ = eng
+    g = golden_chain
+    ref, _ = _run_chain(engine, ms, g, chain_ctl(), 20, shards=1)
+    for shards in (2, 3):
+        got, _ = _run_chain(engine, ms, g, chain_ctl(), 20, shards=shards)
+        for k in ("lon", "lat", "p", "time"):
+            np.testing.assert_array_equal(getattr(got, k), getattr(ref, k))
+
+
+def test_sort_never_changes_results(eng, golden_chain):
+    engine, ms, _ = eng
+    g = golden_chain
+    ref, rc = _run_chain(engine, ms, g, chain_ctl(), 20, shards=1)
+    got, gc = _run_chain(engine, ms, g, chain_ctl(), 20, shards=1, sort_every=3)
+    for k in ("lon", "lat", "p", "time"):
+        np.testing.assert_array_equal(getattr(got, k), getattr(ref, k))
+    np.testing.assert_array_equal(got.q, ref.q)
+    np.testing.assert_array_equal(gc.uvwp, rc.uvwp)
+
+
+def test_sort_permutation_is_stable_argsort_of_oracle_keys(eng):
+    engine, ms, syn = eng
+    m0, m1 = syn.analytic_pair(dlon=5.0, dlat=5.0, nlev=30, t0=0.0, t1=3600.0)
+    ens = syn.particles(50000, seed=9)
+    ens.lon[:1000] = ens.lon[0]   # ties: stability matters
+    ens.lat[:1000] = ens.lat[0]
+    ens.p[:1000] = ens.p[0]
+    e = engine.Engine(device=0)
+    e.upload(ens)
+    e.bind_met(m0, m1)
+    e.sort()
+    ids = e.ctx.ids(0, ens.np)
+    keys = orc.box_keys(orc.Snapshot.like(m0), ens.lon, ens.lat, ens.p)
+    np.testing.assert_array_equal(ids, np.argsort(keys, kind="stable").astype(np.uint32))
+    e.close()
+
+
+def test_sbr_cfg1_whole_run(eng, golden_sbr):
+    """cfg1 shape (1 deg x 60, SBR, 480 steps) against the reference run."""
+    engine, ms, syn = eng
+    g = golden_sbr
+    m0, m1 = syn.solid_body_pair(1.0, 1.0, 60)
+    np.testing.assert_array_equal(m0.lons[:-1], g["lons"])
+    ctl = ms.Control(t_stop=86400.0, dt_model=180.0)
+    ens = _ens(ms, g, "init")
+    e = engine.Engine(device=0)
+    e.upload(ens)
+    e.bind_met(m0, m1)
+    for step in range(480):
+        e.step(ctl, step, engine.ADV)
+    e.download(ens)
+    e.close()
+    np.testing.assert_array_equal(ens.time, g["final_time"])
+    for k in ("lon", "lat", "p"):
+        np.testing.assert_allclose(getattr(ens, k), g[f"final_{k}"], rtol=1e-9, atol=1e-9)
+
+
+def test_met_rotation_matches_oracle(eng):
+    engine, ms, syn = eng
+    lons, lats, levs = syn.grid(10.0, 5.0, 20)
+    mets = [syn.snapshot(3600.0 * k, lons, lats, levs, syn.era5_like(lons, lats, levs, 7.0 * k))
+            for k in range(4)]
+    ctl = ms.Control(t_stop=3 * 3600.0, dt_model=600.0, rng_mode="counter", rng_seed_global=3,
+                     met_dt=3600.0)
+    ens = syn.particles(3000, seed=4)
+    st = {"time": ens.time.copy(), "lon": ens.lon.copy(), "lat": ens.lat.copy(),
+          "p": ens.p.copy(), "uvwp": np.zeros((3, ens.np)), "iso_var": np.zeros(ens.np),
+          "q": np.zeros((5, ens.np))}
+    e = engine.Engine(device=0)
+    e.upload(ens)
+    e.bind_met(mets[0], mets[1])
+    snaps = [orc.Snapshot.like(m) for m in mets]
+    k1, t = 1, 0.0
+    for step in range(18):
+        t_next = min(t + ctl.dt_model, ctl.t_stop)
+        while mets[k1].t_met < t_next:
+            e.prefetch(met=mets[k1 + 1])
+            e.rotate()
+            k1 += 1
+        e.step(ctl, step, engine.ADV_DIFF)
+        orc.full_step(ctl, snaps[k1 - 1], snaps[k1], st, 0, ens.np, step,
+                      modules=("advection", "turb", "meso", "position"))
+        t = t_next
+    got = e.download()
+    e.close()
+    for k in ("lon", "lat", "p", "time"):
+        np.testing.assert_allclose(getattr(got, k), st[k], rtol=1e-10, atol=1e-9)

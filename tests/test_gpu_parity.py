@@ -1,0 +1,312 @@
+"""GPU parity: the drop-in module API (liblagtrans_b200 kernels) against the
+golden vectors made by the reference and against the oracle.
+
+Tolerance contract: cell indices, uint64 RNG words,
+uniforms and every result built only from + - * / sqrt are bit-exact
+(the library is compiled with -fmad=false and keeps numpy's operation
+order); results that pass through cos/log/pow/exp (libdevice vs numpy's
+SIMD libm, ~1 ulp apart) are held to 1e-12 relative per call."""
+
+import numpy as np
+import pytest
+
+from conftest import chain_ctl, control, modules_ctl, snapshot_from
+from oracle import lagtrans_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+ULP = dict(rtol=1e-12, atol=1e-12)
+
+
+@pytest.fixture(scope="module")
+def b200():
+    import paper_2211_12616_b200.physics as phys
+    import paper_2211_12616_b200.rng as rng
+    from paper_2211_12616_b200 import model_state as ms
+    return phys, rng, ms
+
+
+def exact(a, b):
+    np.testing.assert_array_equal(np.asarray(a), np.asarray(b))
+
+
+def host_ensemble(ms, g, tag, nq=5):
+    ens = ms.ParticleEnsemble(np=g[f"{tag}_p"].size, time=g[f"{tag}_time"].copy(),
+                              p=g[f"{tag}_p"].copy(), zeta=g[f"{tag}_zeta"].copy(),
+                              lon=g[f"{tag}_lon"].copy(), lat=g[f"{tag}_lat"].copy(),
+                              q=g[f"{tag}_q"].copy())
+    return ens
+
+
+def cache_from(ms, g, tag):
+    return ms.CacheState(uvwp=g[f"{tag}_uvwp"].copy(), iso_var=g[f"{tag}_iso"].copy())
+
+
+# ------------------------------------------------------------ interpolation
+
+def test_interpolate_met_bit_exact(b200, golden_interp):
+    phys, _, _ = b200
+    g = golden_interp
+    m0, m1 = snapshot_from(g, "m0"), snapshot_from(g, "m1")
+    out = phys.interpolate_met(m0, m1, g["t"], g["lon"], g["lat"], g["p"])
+    exact(np.stack(out), g["uvwT"])
+    same = phys.interpolate_met(m0, m0, g["t"], g["lon"], g["lat"], g["p"])
+    exact(np.stack(same), g["uvwT_same"])
+
+
+def test_interpolate_met_f64_store(b200, golden_interp):
+    """f64 met store on non-fp32 values (reference conftest.make_met style)."""
+    phys, _, _ = b200
+    from paper_2211_12616_b200.physics import default_context
+    g = golden_interp
+    m0 = snapshot_from(g, "m0")
+    m0.u = m0.u + 1e-9 * np.arange(m0.u.size).reshape(m0.u.shape)  # not fp32-representable
+    ctx = default_context()
+    old = ctx.met_precision
+    try:
+        ctx.met_precision = "f64"
+        ctx._grid_key = None
+        (u,) = phys.interpolate_met(m0, m0, 0.0, g["lon"], g["lat"], g["p"], fields=("u",))
+    finally:
+        ctx.met_precision = old
+        ctx._grid_key = None
+    (ref,) = orc.sample(m0, m0, 0.0, g["lon"], g["lat"], g["p"], ("u",))
+    exact(u, ref)
+
+
+# ------------------------------------------------------------ module stages
+
+@pytest.fixture(scope="module")
+def mods(golden_modules):
+    g = golden_modules
+    return g, modules_ctl(), snapshot_from(g, "m0"), snapshot_from(g, "m1")
+
+
+def _batch(rng, g):
+    b = rng.batch_allocate(int(g["n"]))
+    b.convection[:] = g["rnd_conv"]
+    b.diff_turb[:] = g["rnd_turb"]
+    b.diff_meso[:] = g["rnd_meso"]
+    return b
+
+
+def _work(g):
+    from paper_2211_12616_b200.partition import WorkRange
+    return WorkRange(0, 0, int(g["n"]))
+
+
+def test_module_timesteps(b200, mods):
+    phys, _, ms = b200
+    g, ctl, m0, m1 = mods
+    ens = host_ensemble(ms, g, "isoinit")
+    dt = np.zeros(ens.np)
+    phys.module_timesteps(ctl, ens, 0.0, _work(g), dt)
+    exact(dt, g["timesteps_dt"])
+
+
+def test_module_isosurf_init(b200, mods):
+    phys, _, ms = b200
+    g, ctl, m0, m1 = mods
+    ens = host_ensemble(ms, g, "timesteps")
+    cache = cache_from(ms, g, "timesteps")
+    phys.module_isosurf_init(ctl, ens, m0, m1, cache, _work(g))
+    np.testing.assert_allclose(cache.iso_var, g["isoinit_iso"], **ULP)
+
+
+def test_module_advection(b200, mods):
+    phys, _, ms = b200
+    g, ctl, m0, m1 = mods
+    ens = host_ensemble(ms, g, "isoinit")
+    phys.module_advection(ctl, ens, m0, m1, g["isoinit_dt"].copy(), _work(g))
+    for k in ("lon", "lat", "p"):
+        np.testing.assert_allclose(getattr(ens, k), g[f"advection_{k}"], **ULP)
+    exact(ens.time, g["advection_time"])
+    # lat/p only see cos through the midpoint longitude: almost all bit-exact
+    assert np.mean(ens.lat == g["advection_lat"]) > 0.9
+
+
+def test_module_turb(b200, mods):
+    phys, rng, ms = b200
+    g, ctl, m0, m1 = mods
+    ens = host_ensemble(ms, g, "advection")
+    phys.module_diffusion_turb(ctl, ens, m0, m1, g["advection_dt"].copy(), _batch(rng, g), _work(g))
+    for k in ("lon", "lat", "p"):
+        np.testing.assert_allclose(getattr(ens, k), g[f"turb_{k}"], **ULP)
+    exact(ens.lat, g["turb_lat"])
+
+
+def test_module_meso(b200, mods):
+    phys, rng, ms = b200
+    g, ctl, m0, m1 = mods
+    ens = host_ensemble(ms, g, "turb")
+    cache = cache_from(ms, g, "turb")
+    phys.module_diffusion_meso(ctl, ens, m0, m1, g["turb_dt"].copy(), _batch(rng, g), cache, _work(g))
+    exact(cache.uvwp, g["meso_uvwp"])
+    exact(ens.lat, g["meso_lat"])
+    exact(ens.p, g["meso_p"])
+    np.testing.assert_allclose(ens.lon, g["meso_lon"], **ULP)
+
+
+def test_module_convection(b200, mods):
+    phys, rng, ms = b200
+    g, ctl, m0, m1 = mods
+    ens = host_ensemble(ms, g, "meso")
+    phys.module_convection(ctl, ens, g["meso_dt"].copy(), _batch(rng, g), _work(g))
+    exact(ens.p, g["convection_p"])
+
+
+def test_module_sedi(b200, mods):
+    phys, _, ms = b200
+    g, ctl, m0, m1 = mods
+    ens = host_ensemble(ms, g, "convection")
+    phys.module_sedi(ctl, ens, m0, m1, g["convection_dt"].copy(), _work(g))
+    exact(ens.p, g["sedi_p"])
+
+
+def test_module_isosurf_theta(b200, mods):
+    phys, _, ms = b200
+    g, ctl, m0, m1 = mods
+    ens = host_ensemble(ms, g, "preiso")
+    cache = cache_from(ms, g, "preiso")
+    cache.iso_nonconverged = 0
+    phys.module_isosurf(ctl, ens, m0, m1, cache, _work(g))
+    np.testing.assert_allclose(ens.p, g["isosurf_p"], rtol=1e-10, atol=1e-10)
+    assert cache.iso_nonconverged == int(g["iso_nonconverged"])
+
+
+def test_module_position(b200, mods):
+    phys, _, ms = b200
+    g, ctl, m0, m1 = mods
+    ens = host_ensemble(ms, g, "preposition")
+    phys.module_position(ctl, ens, _work(g))
+    exact(ens.lon, g["position_lon"])
+    exact(ens.lat, g["position_lat"])
+    exact(ens.p, g["position_p"])
+
+
+def test_module_meteo(b200, mods):
+    phys, _, ms = b200
+    g, ctl, m0, m1 = mods
+    ens = host_ensemble(ms, g, "position")
+    phys.module_meteo(ctl, ens, m0, m1, ms.read_clim(ctl), _work(g))
+    np.testing.assert_allclose(ens.q[:5], g["meteo_q"][:5], **ULP)
+    exact(ens.q[4], g["meteo_q"][4])
+
+
+def test_module_isosurf_pressure(b200, mods):
+    phys, _, ms = b200
+    g, _, m0, m1 = mods
+    ctl = control(isosurf_mode="pressure")
+    ens = host_ensemble(ms, g, "meteo")
+    cache = cache_from(ms, g, "meteo")
+    phys.module_isosurf_init(ctl, ens, m0, m1, cache, _work(g))
+    ens.p[:] = ens.p + 3.0
+    phys.module_isosurf(ctl, ens, m0, m1, cache, _work(g))
+    exact(ens.p, g["isopressure_p"])
+
+
+def test_range_purity_and_subrange(b200, mods):
+    """physics.py:1-7: a module on [a, b) leaves every byte outside unchanged
+    and equals the whole-range result inside."""
+    phys, rng, ms = b200
+    from paper_2211_12616_b200.partition import WorkRange
+    g, ctl, m0, m1 = mods
+    ens = host_ensemble(ms, g, "isoinit")
+    before = ens.lon.copy(), ens.lat.copy(), ens.p.copy(), ens.time.copy()
+    dt = g["isoinit_dt"].copy()
+    phys.module_advection(ctl, ens, m0, m1, dt, WorkRange(0, 700, 1900))
+    out = np.r_[0:700, 1900:ens.np]
+    for a, b in zip((ens.lon, ens.lat, ens.p, ens.time), before):
+        exact(a[out], b[out])
+    whole = host_ensemble(ms, g, "isoinit")
+    phys.module_advection(ctl, whole, m0, m1, dt, _work(g))
+    exact(ens.lon[700:1900], whole.lon[700:1900])
+    exact(ens.p[700:1900], whole.p[700:1900])
+
+
+# ------------------------------------------------------------ random numbers
+
+def test_counter_batch(b200, golden_rng):
+    _, rng, ms = b200
+    from paper_2211_12616_b200.partition import partition_all
+    g = golden_rng
+    ctl = ms.Control(rng_mode="counter", rng_seed_global=99)
+    st = rng.module_rng_init(ctl, 3)
+    b = rng.batch_allocate(1000)
+    for w in partition_all(1000, 3):
+        rng.generate_random_nums(st, 7, w, w.device_id, b)
+    exact(b.convection, g["counter_conv"])
+    np.testing.assert_allclose(b.diff_turb, g["counter_turb"], rtol=1e-13, atol=1e-13)
+    np.testing.assert_allclose(b.diff_meso, g["counter_meso"], rtol=1e-13, atol=1e-13)
+
+
+def test_faithful_batch(b200, golden_rng):
+    _, rng, ms = b200
+    from paper_2211_12616_b200.partition import partition_all
+    g = golden_rng
+    ctl = ms.Control(rng_mode="faithful", mpi_rank=3)
+    st = rng.module_rng_init(ctl, 2)
+    b = rng.batch_allocate(1000)
+    w0, w1 = partition_all(1000, 2)
+    rng.generate_random_nums(st, 0, w1, 1, b)
+    rng.generate_random_nums(st, 1, w1, 1, b)
+    assert st.device_states[1] == int(g["faithful_state_out"])
+    lo, hi = int(g["faithful_start"]), int(g["faithful_end"])
+    exact(b.convection[lo:hi], g["faithful_conv"][lo:hi])
+    np.testing.assert_allclose(b.diff_turb, g["faithful_turb"], rtol=1e-13, atol=1e-13)
+    np.testing.assert_allclose(b.diff_meso, g["faithful_meso"], rtol=1e-13, atol=1e-13)
+
+
+def test_philox_moments(b200):
+    """Fast mode matches distributionally (test_rng.py:157-165 bounds)."""
+    _, rng, ms = b200
+    from paper_2211_12616_b200.partition import WorkRange
+    n = 10 ** 6
+    st = rng.RngState("philox", 5)
+    b = rng.batch_allocate(n)
+    rng.generate_random_nums(st, 0, WorkRange(0, 0, n), 0, b)
+    assert abs(b.convection.mean() - 0.5) < 0.002
+    assert b.convection.min() >= 0.0 and b.convection.max() < 1.0
+    for arr in (b.diff_turb, b.diff_meso):
+        assert abs(arr.mean()) < 0.004
+        assert abs(arr.var() - 1.0) < 0.01
+
+
+# ------------------------------------------------------------ whole chains
+
+def _module_chain(phys, rng, ms, ctl, g, m0, m1, steps, parts):
+    from paper_2211_12616_b200.partition import partition_all
+    ens = host_ensemble(ms, g, "init")
+    n = ens.np
+    cache = ms.cache_allocate(n)
+    dt = np.zeros(n)
+    batch = rng.batch_allocate(n)
+    clim = ms.read_clim(ctl)
+    st = rng.module_rng_init(ctl, parts)
+    ranges = partition_all(n, parts)
+    for w in ranges:
+        phys.module_isosurf_init(ctl, ens, m0, m1, cache, w)
+    for step in range(steps):
+        for w in ranges:
+            phys.module_timesteps(ctl, ens, 0.0, w, dt)
+            rng.generate_random_nums(st, step, w, w.device_id, batch)
+            phys.module_advection(ctl, ens, m0, m1, dt, w)
+            phys.module_diffusion_turb(ctl, ens, m0, m1, dt, batch, w)
+            phys.module_diffusion_meso(ctl, ens, m0, m1, dt, batch, cache, w)
+            phys.module_convection(ctl, ens, dt, batch, w)
+            phys.module_sedi(ctl, ens, m0, m1, dt, w)
+            phys.module_isosurf(ctl, ens, m0, m1, cache, w)
+            phys.module_position(ctl, ens, w)
+            phys.module_meteo(ctl, ens, m0, m1, clim, w)
+    return ens, cache
+
+
+def test_chain_50_steps_module_api(b200, golden_chain):
+    phys, rng, ms = b200
+    g = golden_chain
+    m0, m1 = snapshot_from(g, "m0"), snapshot_from(g, "m1")
+    ens, cache = _module_chain(phys, rng, ms, chain_ctl(), g, m0, m1, 50, parts=2)
+    exact(ens.time, g["final_time"])
+    for k in ("lon", "lat", "p"):
+        np.testing.assert_allclose(getattr(ens, k), g[f"final_{k}"], rtol=1e-9, atol=1e-9)
+    np.testing.assert_allclose(ens.q, g["final_q"], rtol=1e-9, atol=1e-9)
