@@ -42,32 +42,40 @@ def _stale() -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, outdir: Path | None = None,
+          defines: tuple[str, ...] = ()) -> Path:
+    """Compile and link; `outdir`/`defines` build an experimental variant."""
+    libdir = Path(outdir) if outdir else LIBDIR
+    lib = libdir / LIB.name
+    if not force and outdir is None and not defines and not _stale():
         return LIB
-    LIBDIR.mkdir(exist_ok=True)
+    libdir.mkdir(parents=True, exist_ok=True)
     objs = []
     log = []
     for src in SOURCES:
-        obj = LIBDIR / (Path(src).stem + ".o")
-        cmd = [nvcc(), *ARCH, *FLAGS, "-I", str(PKG.parent / "include"), "-c",
+        obj = libdir / (Path(src).stem + ".o")
+        cmd = [nvcc(), *ARCH, *FLAGS, *[f"-D{d}" for d in defines],
+               "-I", str(PKG.parent / "include"), "-c",
                str(CSRC / src), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         log.append(r.stdout + r.stderr)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n{r.stderr}")
         objs.append(str(obj))
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [nvcc(), *ARCH, "-shared", "--cudart", "static", "-o", str(tmp), *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
-    os.replace(tmp, LIB)
-    (LIBDIR / "ptxas.log").write_text("\n".join(log))
+    os.replace(tmp, lib)
+    (libdir / "ptxas.log").write_text("\n".join(log))
     if verbose:
         print("\n".join(log))
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    args = sys.argv[1:]
+    defs = tuple(a[2:] for a in args if a.startswith("-D"))
+    out = next((a.split("=", 1)[1] for a in args if a.startswith("--out=")), None)
+    print(build(force="--force" in args, verbose="-v" in args, outdir=out, defines=defs))

@@ -41,6 +41,7 @@ int fail(int code, const char* fmt, ...) {
 
 struct AxisHost {
   double* dev = nullptr;
+  double lo = 0.0, hi = 0.0;
   int n = 0;
   int logscale = 0;
   float g0 = 0.f, ginv = 0.f;
@@ -132,6 +133,8 @@ int upload_axis(AxisHost& ax, const double* x, int n, cudaStream_t st) {
   const double b = ax.logscale ? log2(x[n - 1]) : x[n - 1];
   ax.g0 = static_cast<float>(a);
   ax.ginv = static_cast<float>((n - 1) / (b - a));
+  ax.lo = x[0];
+  ax.hi = x[n - 1];
   if (ax.dev && ax.n != n) {
     cudaFree(ax.dev);
     ax.dev = nullptr;
@@ -149,6 +152,8 @@ int upload_axis(AxisHost& ax, const double* x, int n, cudaStream_t st) {
 Axis view(const AxisHost& a) {
   Axis v;
   v.x = a.dev;
+  v.lo = a.lo;
+  v.hi = a.hi;
   v.n = a.n;
   v.logscale = a.logscale;
   v.g0 = a.g0;
@@ -446,6 +451,8 @@ int lt_met_grid(lt_ctx* c, int32_t nx, int32_t ny, int32_t nz, const double* lon
   if (nx < 2 || ny < 2 || nz < 2) return fail(LT_ERR_ARG, "meteo grid needs nx, ny, nz >= 2");
   if (precision != LT_MET_F32 && precision != LT_MET_F64)
     return fail(LT_ERR_ARG, "met precision must be 4 or 8 bytes");
+  if (static_cast<int64_t>(nx) * ny * (nz - 1) >= (int64_t(1) << 32))
+    return fail(LT_ERR_ARG, "met grid too large: cell records must fit 32-bit indices");
   std::vector<double> asc(levs, levs + nz);
   for (int k = 1; k < nz; ++k)
     if (!(levs[k] < levs[k - 1])) return fail(LT_ERR_ARG, "pressure levels must be strictly decreasing");

@@ -78,7 +78,7 @@ __global__ void box_key_kernel(MetView<Rec> m, const double* lon, const double* 
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t s = start + t;
     const Cell c = cell_of(m, lon[s], lat[s], p[s]);
-    keys[t] = static_cast<uint32_t>(c.r00);
+    keys[t] = c.r00;
     vals[t] = static_cast<uint32_t>(t);
   }
 }

@@ -40,8 +40,37 @@ struct StepArgs {
   Clim clim;
 };
 
+#ifndef LT_STEP_MIN_BLOCKS
+#define LT_STEP_MIN_BLOCKS 3
+#endif
+
+// Draws of one stream for particle slot s / global id gid: stream 0 = the
+// convection uniform (x[0]), 1 = turbulent normals, 2 = mesoscale normals.
+template <class Rec>
+__device__ __forceinline__ void draws(const StepArgs<Rec>& a, int64_t s, uint64_t gid, int stream,
+                                      double x[3]) {
+  if (!(a.flags & F_RNG_INKERNEL)) {  // the caller's RandomBatch
+    if (stream == 0) {
+      x[0] = a.rnd_conv[s];
+    } else {
+      const double* b = stream == 1 ? a.rnd_turb : a.rnd_meso;
+      x[0] = b[3 * s]; x[1] = b[3 * s + 1]; x[2] = b[3 * s + 2];
+    }
+    return;
+  }
+  const Control& ctl = a.ctl;
+  if (ctl.rng_mode == RNG_COUNTER) {
+    if (stream == 0) x[0] = to_unit(counter_word(ctl.rng_seed_global, a.step, gid, 0, 0));
+    else counter_normals(ctl.rng_seed_global, a.step, gid, stream, x);
+  } else if (ctl.rng_mode == RNG_FAITHFUL) {
+    faithful_stream(a.faithful_state, gid - static_cast<uint64_t>(a.faithful_base), stream, x);
+  } else {
+    philox_stream(ctl.rng_seed_global, a.step, gid, stream, x);
+  }
+}
+
 template <class Rec, uint32_t FIXED>
-__global__ void __launch_bounds__(256) step_kernel(const StepArgs<Rec> a) {
+__global__ void __launch_bounds__(256, LT_STEP_MIN_BLOCKS) step_kernel(const StepArgs<Rec> a) {
   const uint32_t mods = FIXED ? FIXED : a.modules;
   const Control& ctl = a.ctl;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -62,30 +91,14 @@ __global__ void __launch_bounds__(256) step_kernel(const StepArgs<Rec> a) {
     }
     const bool act = dt > 0.0;
 
-    // random draws: rng.py:156-181 (in-kernel) or the caller's RandomBatch
+    // random draws (rng.py:156-181) are made where they are consumed, which
+    // keeps them out of the registers live across the advection gathers
     const bool want_turb = (mods & M_TURB) && (ctl.turb_dx != 0.0 || ctl.turb_dz != 0.0);
     const bool want_meso = (mods & M_MESO) && ctl.turb_meso != 0.0;
     const bool want_conv = (mods & M_CONVECTION) && ctl.conv_prob != 0.0;
-    double xc = 0.0, xt[3] = {0.0, 0.0, 0.0}, xm[3] = {0.0, 0.0, 0.0};
-    if (want_turb || want_meso || want_conv) {
-      if (a.flags & F_RNG_INKERNEL) {
-        const uint64_t gid = a.ids ? static_cast<uint64_t>(a.ids[s]) : static_cast<uint64_t>(s);
-        if (ctl.rng_mode == RNG_COUNTER) {
-          const uint64_t seed = ctl.rng_seed_global;
-          if (want_conv) xc = to_unit(counter_word(seed, a.step, gid, 0, 0));
-          if (want_turb) counter_normals(seed, a.step, gid, 1, xt);
-          if (want_meso) counter_normals(seed, a.step, gid, 2, xm);
-        } else if (ctl.rng_mode == RNG_FAITHFUL) {
-          faithful_draws(a.faithful_state, gid - static_cast<uint64_t>(a.faithful_base), xc, xt, xm);
-        } else {
-          philox_draws(ctl.rng_seed_global, a.step, gid, xc, xt, xm);
-        }
-      } else {
-        if (want_conv) xc = a.rnd_conv[s];
-        if (want_turb) { xt[0] = a.rnd_turb[3 * s]; xt[1] = a.rnd_turb[3 * s + 1]; xt[2] = a.rnd_turb[3 * s + 2]; }
-        if (want_meso) { xm[0] = a.rnd_meso[3 * s]; xm[1] = a.rnd_meso[3 * s + 1]; xm[2] = a.rnd_meso[3 * s + 2]; }
-      }
-    }
+    const uint64_t gid = (a.flags & F_RNG_INKERNEL) && (want_turb || want_meso || want_conv)
+                             ? (a.ids ? static_cast<uint64_t>(a.ids[s]) : static_cast<uint64_t>(s))
+                             : 0ull;
 
     // physics.py:225-235 (module_isosurf_init)
     if ((mods & M_ISOSURF_INIT) && ctl.isosurf_mode != ISO_OFF) {
@@ -116,6 +129,8 @@ __global__ void __launch_bounds__(256) step_kernel(const StepArgs<Rec> a) {
     // physics.py:119-147 (module_diffusion_turb); the vertical part sees the
     // post-hop lon/lat and pre-hop p (numpy view aliasing)
     if (want_turb && act) {
+      double xt[3];
+      draws(a, s, gid, 1, xt);
       if (ctl.turb_dx > 0.0) {
         const double sig = sqrt(2.0 * ctl.turb_dx * dt);
         const double nlon = lon + sig * xt[0] * kDegPerM / cos_lat(lat);
@@ -133,6 +148,8 @@ __global__ void __launch_bounds__(256) step_kernel(const StepArgs<Rec> a) {
 
     // physics.py:150-188 (module_diffusion_meso): AR(1) with met0 cell spread
     if (want_meso && act) {
+      double xm[3];
+      draws(a, s, gid, 2, xm);
       const Cell c = cell_of(a.met, lon, lat, p);
       Corners<Rec> q;
       gather(a.met.s0, a.met, c.r00, q);
@@ -153,8 +170,12 @@ __global__ void __launch_bounds__(256) step_kernel(const StepArgs<Rec> a) {
     }
 
     // physics.py:191-203 (module_convection)
-    if (want_conv && act && p > ctl.conv_p_top && xc < ctl.conv_prob)
-      p = ctl.conv_p_top + (xc / ctl.conv_prob) * (ctl.p_surf - ctl.conv_p_top);
+    if (want_conv && act) {
+      double xc[3];
+      draws(a, s, gid, 0, xc);
+      if (p > ctl.conv_p_top && xc[0] < ctl.conv_prob)
+        p = ctl.conv_p_top + (xc[0] / ctl.conv_prob) * (ctl.p_surf - ctl.conv_p_top);
+    }
 
     // physics.py:206-222 (module_sedi): Stokes settling
     if ((mods & M_SEDI) && ctl.sedi_radius != 0.0 && act) {
