@@ -162,9 +162,14 @@ def load_met_everywhere(eng, mets, ws, rank, torch, dist):
     return None, None
 
 
-def cpu_sample_rate(wl, mets, ctl, n_sample, steps, threads):
+def cpu_sample_rate(wl, mets, ctl, n_sample, steps, threads, target_s=0.0):
     """The CPU oracle on `threads` host threads over a particle sample
-    (DevicePool-style static partition); returns particle-steps/s."""
+    (DevicePool-style static partition); returns (particle-steps/s, wall s,
+    sample size).  With target_s > 0 the sample is sized from a probe so the
+    timed steps take about target_s seconds."""
+    if target_s > 0:
+        probe, _, _ = cpu_sample_rate(wl, mets, ctl, n_sample, 1, threads)
+        n_sample = int(min(max(probe * target_s / steps, 10_000), 20_000_000))
     from concurrent.futures import ThreadPoolExecutor
 
     from oracle import lagtrans_oracle as orc
@@ -188,14 +193,14 @@ def cpu_sample_rate(wl, mets, ctl, n_sample, steps, threads):
         for k in range(steps):
             one(1 + k)
         wall = time.perf_counter() - t0
-    return n_sample * steps / wall, wall
+    return n_sample * steps / wall, wall, n_sample
 
 
-def make_ctl(wl):
+def make_ctl(wl, precision="exact"):
     from paper_2211_12616_b200.model_state import Control
     return Control(np_max=10 ** 10, t_stop=10 * 86400.0, dt_model=180.0, met_dt=10800.0,
                    turb_dx=50.0, turb_dz=0.1, turb_meso=0.16, rng_mode="counter",
-                   rng_seed_global=12616)
+                   rng_seed_global=12616, precision=precision)
 
 
 def host_threads():
@@ -216,10 +221,11 @@ def run_reference(args, wl):
     threads = host_threads()
     n_sample = args.cpu_sample or (100_000 if wl == "cfg1" else 20_000 * threads)
     rates = []
-    for _ in range(max(1, args.steps // 10)):
-        r, _ = cpu_sample_rate(wl, mets, ctl, n_sample, 2, threads)
+    for _ in range(max(1, min(3, args.steps // 10))):
+        r, wall, n_used = cpu_sample_rate(wl, mets, ctl, n_sample, 2, threads, target_s=10.0)
         rates.append(r)
     v = statistics.median(rates)
+    n_sample = n_used
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "particle-steps/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -245,6 +251,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-sample", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--precision", default="exact", choices=("exact", "fast"))
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     wl = args.workload
@@ -266,7 +273,7 @@ def main():
     n_tot, dlon, dlat, nlev, pmin, mod, desc = WORKLOADS[wl]
     mask = engine.ADV if mod == "adv" else engine.ADV_DIFF
     work = calc_device_workload_range(n_tot, ws, rank)
-    ctl = make_ctl(wl)
+    ctl = make_ctl(wl, args.precision)
 
     mets = build_met(wl, rank, ws, torch, dist)
     eng = engine.Engine(device=local, first_id=work.start)
@@ -367,7 +374,8 @@ def main():
         threads = host_threads()
         n_sample = args.cpu_sample or (100_000 if wl == "cfg1" else 20_000 * threads)
         mh = mets if wl == "cfg1" else (m0, m1)
-        rate, wall = cpu_sample_rate(wl, mh, ctl, n_sample, 2, threads)
+        rate, wall, n_sample = cpu_sample_rate(wl, mh, make_ctl(wl), n_sample, 2, threads,
+                                               target_s=15.0)
         cpu = {"value": rate, "unit": "particle-steps/s", "cores": threads, "kind": "port",
                "sample": f"oracle/ numpy port, {n_sample} particles x 2 timed steps on the "
                          f"same {wl} met grid ({wall:.1f} s)"}
@@ -382,6 +390,7 @@ def main():
             "config": {"workload": wl, "description": desc, "particles": n_tot,
                        "particles_per_gpu": work.size, "met_nodes": nodes,
                        "met_store": "fp32 node-pair records", "state": "fp64 SoA",
+                       "precision": args.precision,
                        "rng": "counter (bit-identical to reference), in-kernel",
                        "sort_every": sort_every, "parallelism": f"particles sharded x{ws}",
                        "l2": "inputs larger than L2 (state %.1f GB/GPU)" % (

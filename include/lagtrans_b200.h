@@ -111,7 +111,7 @@ typedef struct lt_control {
   int32_t rng_mode;          /* LT_RNG_*  */
   uint64_t rng_seed_global;  /* counter / philox key */
   int32_t decay_slot;        /* q row decayed by LT_MOD_DECAY */
-  int32_t reserved;
+  int32_t precision;         /* 0 exact (bit-faithful fp64), 1 fast (mixed) */
 } lt_control;
 
 typedef struct lt_ctx lt_ctx;

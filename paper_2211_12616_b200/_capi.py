@@ -37,6 +37,7 @@ RUN_WRITE_DT = 1 << 2
 
 RNG_MODES = {"faithful": 0, "counter": 1, "philox": 2}
 ISO_MODES = {"off": 0, "pressure": 1, "theta": 2}
+PRECISIONS = {"exact": 0, "fast": 1}
 
 F_TIME, F_P, F_ZETA, F_LON, F_LAT, F_Q, F_UVWP, F_ISO_VAR, F_DT = range(9)
 F_RND_CONV, F_RND_TURB, F_RND_MESO, F_ID = 9, 10, 11, 12
@@ -63,7 +64,7 @@ class LtControl(C.Structure):
                 ("sedi_density", C.c_double), ("decay_tau", C.c_double),
                 ("isosurf_mode", C.c_int32), ("rng_mode", C.c_int32),
                 ("rng_seed_global", C.c_uint64), ("decay_slot", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("precision", C.c_int32)]
 
 
 def control_struct(ctl) -> LtControl:
@@ -80,7 +81,8 @@ def control_struct(ctl) -> LtControl:
                      float(ctl.p_top), float(ctl.sedi_radius), float(ctl.sedi_density),
                      float(getattr(ctl, "decay_tau", 0.0)), ISO_MODES[iso], RNG_MODES[mode],
                      int(ctl.rng_seed_global) & 0xFFFFFFFFFFFFFFFF,
-                     int(getattr(ctl, "decay_slot", -1)), 0)
+                     int(getattr(ctl, "decay_slot", -1)),
+                     PRECISIONS[getattr(ctl, "precision", "exact")])
 
 
 _P = C.c_void_p

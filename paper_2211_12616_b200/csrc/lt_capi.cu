@@ -41,6 +41,7 @@ int fail(int code, const char* fmt, ...) {
 
 struct AxisHost {
   double* dev = nullptr;
+  float* rdx = nullptr;  // fp32 reciprocal cell widths
   double lo = 0.0, hi = 0.0;
   int n = 0;
   int logscale = 0;
@@ -137,14 +138,21 @@ int upload_axis(AxisHost& ax, const double* x, int n, cudaStream_t st) {
   ax.hi = x[n - 1];
   if (ax.dev && ax.n != n) {
     cudaFree(ax.dev);
+    cudaFree(ax.rdx);
     ax.dev = nullptr;
+    ax.rdx = nullptr;
   }
   ax.n = n;
   if (!ax.dev) {
     int rc = alloc_dev(reinterpret_cast<void**>(&ax.dev), sizeof(double) * n, "axis");
     if (rc) return rc;
+    rc = alloc_dev(reinterpret_cast<void**>(&ax.rdx), sizeof(float) * n, "axis rdx");
+    if (rc) return rc;
   }
+  std::vector<float> rdx(n, 0.0f);
+  for (int i = 0; i + 1 < n; ++i) rdx[i] = static_cast<float>(1.0 / (x[i + 1] - x[i]));
   CK(cudaMemcpyAsync(ax.dev, x, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(ax.rdx, rdx.data(), sizeof(float) * n, cudaMemcpyHostToDevice, st));
   CK(cudaStreamSynchronize(st));
   return LT_OK;
 }
@@ -152,6 +160,7 @@ int upload_axis(AxisHost& ax, const double* x, int n, cudaStream_t st) {
 Axis view(const AxisHost& a) {
   Axis v;
   v.x = a.dev;
+  v.rdx = a.rdx;
   v.lo = a.lo;
   v.hi = a.hi;
   v.n = a.n;
@@ -176,6 +185,7 @@ MetView<Rec> met_view(const lt_ctx* c) {
   m.s1 = static_cast<const Rec*>(c->slots[c->use1].rec);
   m.t0 = c->slots[c->use0].t_met;
   m.t1 = c->slots[c->use1].t_met;
+  m.inv_dt = m.t1 != m.t0 ? 1.0 / (m.t1 - m.t0) : 0.0;
   return m;
 }
 
@@ -303,7 +313,10 @@ int lt_ctx_destroy(lt_ctx* c) {
     cudaEventDestroy(s.ready);
   }
   free_dev(c->staging);
-  for (AxisHost* a : {&c->ax_lon, &c->ax_lat, &c->ax_lev, &c->cl_lat, &c->cl_p}) free_dev(a->dev);
+  for (AxisHost* a : {&c->ax_lon, &c->ax_lat, &c->ax_lev, &c->cl_lat, &c->cl_p}) {
+    free_dev(a->dev);
+    free_dev(a->rdx);
+  }
   free_dev(c->hno3);
   free_dev(c->p_trop);
   free_dev(c->counters);

@@ -9,7 +9,7 @@ namespace lt {
 constexpr uint32_t kChainAdv = M_TIMESTEPS | M_ADVECTION | M_POSITION;
 constexpr uint32_t kChainAdvDiff = M_TIMESTEPS | M_ADVECTION | M_TURB | M_MESO | M_POSITION;
 
-template <class Rec, uint32_t FIXED>
+template <class Rec, uint32_t FIXED, bool FAST>
 static cudaError_t launch_fixed(const StepArgs<Rec>& a, cudaStream_t st) {
   static int blocks_per_sm = 0;
   static int sms = 0;
@@ -17,7 +17,7 @@ static cudaError_t launch_fixed(const StepArgs<Rec>& a, cudaStream_t st) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, step_kernel<Rec, FIXED>, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, step_kernel<Rec, FIXED, FAST>, 256, 0);
     if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
   const int64_t n = a.end - a.start;
@@ -25,15 +25,22 @@ static cudaError_t launch_fixed(const StepArgs<Rec>& a, cudaStream_t st) {
   int64_t grid = (n + 255) / 256;
   const int64_t cap = static_cast<int64_t>(sms) * blocks_per_sm * 16;
   if (grid > cap) grid = cap;
-  step_kernel<Rec, FIXED><<<static_cast<unsigned>(grid), 256, 0, st>>>(a);
+  step_kernel<Rec, FIXED, FAST><<<static_cast<unsigned>(grid), 256, 0, st>>>(a);
   return cudaGetLastError();
+}
+
+template <class Rec, bool FAST>
+static cudaError_t launch_prec(const StepArgs<Rec>& a, cudaStream_t st) {
+  if (a.modules == kChainAdvDiff) return launch_fixed<Rec, kChainAdvDiff, FAST>(a, st);
+  if (a.modules == kChainAdv) return launch_fixed<Rec, kChainAdv, FAST>(a, st);
+  return launch_fixed<Rec, 0, FAST>(a, st);
 }
 
 template <class Rec>
 cudaError_t launch_step(const StepArgs<Rec>& a, cudaStream_t st) {
-  if (a.modules == kChainAdvDiff) return launch_fixed<Rec, kChainAdvDiff>(a, st);
-  if (a.modules == kChainAdv) return launch_fixed<Rec, kChainAdv>(a, st);
-  return launch_fixed<Rec, 0>(a, st);
+  // the fast (mixed-precision) kernels exist for the fp32 met store only
+  if (a.ctl.precision == 1 && sizeof(Rec) == sizeof(RecF)) return launch_prec<Rec, true>(a, st);
+  return launch_prec<Rec, false>(a, st);
 }
 template cudaError_t launch_step<RecF>(const StepArgs<RecF>&, cudaStream_t);
 template cudaError_t launch_step<RecD>(const StepArgs<RecD>&, cudaStream_t);

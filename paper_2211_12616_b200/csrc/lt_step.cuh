@@ -44,9 +44,46 @@ struct StepArgs {
 #define LT_STEP_MIN_BLOCKS 3
 #endif
 
+// Arithmetic policy: EXACT reproduces numpy's operation sequence in fp64;
+// FAST is the mixed-precision path of lt_device.cuh (fp32 store only).
+template <class Rec, bool FAST>
+struct Ops {
+  static constexpr bool kFast = false;
+  __device__ static void sample(const MetView<Rec>& m, double t, double lon, double lat,
+                                double p, int fmask, double out[4]) {
+    lt::sample(m, t, lon, lat, p, fmask, out);
+  }
+  __device__ static double over_cos(double x, double lat) { return x / cos_lat(lat); }
+  __device__ static uint32_t cell(const MetView<Rec>& m, double lon, double lat, double p) {
+    return cell_of(m, lon, lat, p).r00;
+  }
+  template <class T>
+  __device__ static double spread(const CornersT<T>& q, int f) { return corner_std(q, f); }
+  __device__ static void normals(uint64_t seed, int64_t step, uint64_t gid, int stream, double z[3]) {
+    counter_normals(seed, step, gid, stream, z);
+  }
+};
+
+template <>
+struct Ops<RecF, true> {
+  static constexpr bool kFast = true;
+  __device__ static void sample(const MetView<RecF>& m, double t, double lon, double lat,
+                                double p, int fmask, double out[4]) {
+    sample_fast(m, t, lon, lat, p, fmask, out);
+  }
+  __device__ static double over_cos(double x, double lat) { return x * inv_cos_lat_fast(lat); }
+  __device__ static uint32_t cell(const MetView<RecF>& m, double lon, double lat, double p) {
+    return cell_fast(m, lon, lat, p).r00;
+  }
+  __device__ static double spread(const CornersT<float>& q, int f) { return corner_std_f(q, f); }
+  __device__ static void normals(uint64_t seed, int64_t step, uint64_t gid, int stream, double z[3]) {
+    counter_normals_fast(seed, step, gid, stream, z);
+  }
+};
+
 // Draws of one stream for particle slot s / global id gid: stream 0 = the
 // convection uniform (x[0]), 1 = turbulent normals, 2 = mesoscale normals.
-template <class Rec>
+template <class O, class Rec>
 __device__ __forceinline__ void draws(const StepArgs<Rec>& a, int64_t s, uint64_t gid, int stream,
                                       double x[3]) {
   if (!(a.flags & F_RNG_INKERNEL)) {  // the caller's RandomBatch
@@ -61,7 +98,7 @@ __device__ __forceinline__ void draws(const StepArgs<Rec>& a, int64_t s, uint64_
   const Control& ctl = a.ctl;
   if (ctl.rng_mode == RNG_COUNTER) {
     if (stream == 0) x[0] = to_unit(counter_word(ctl.rng_seed_global, a.step, gid, 0, 0));
-    else counter_normals(ctl.rng_seed_global, a.step, gid, stream, x);
+    else O::normals(ctl.rng_seed_global, a.step, gid, stream, x);
   } else if (ctl.rng_mode == RNG_FAITHFUL) {
     faithful_stream(a.faithful_state, gid - static_cast<uint64_t>(a.faithful_base), stream, x);
   } else {
@@ -69,8 +106,9 @@ __device__ __forceinline__ void draws(const StepArgs<Rec>& a, int64_t s, uint64_
   }
 }
 
-template <class Rec, uint32_t FIXED>
+template <class Rec, uint32_t FIXED, bool FAST>
 __global__ void __launch_bounds__(256, LT_STEP_MIN_BLOCKS) step_kernel(const StepArgs<Rec> a) {
+  using O = Ops<Rec, FAST>;
   const uint32_t mods = FIXED ? FIXED : a.modules;
   const Control& ctl = a.ctl;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -106,7 +144,7 @@ __global__ void __launch_bounds__(256, LT_STEP_MIN_BLOCKS) step_kernel(const Ste
         a.iso_var[s] = p;
       } else {
         double v[4];
-        sample(a.met, time, lon, lat, p, 8, v);
+        O::sample(a.met, time, lon, lat, p, 8, v);
         a.iso_var[s] = v[3] * pow(1000.0 / p, kKappa);
       }
     }
@@ -114,13 +152,13 @@ __global__ void __launch_bounds__(256, LT_STEP_MIN_BLOCKS) step_kernel(const Ste
     // physics.py:91-116 (module_advection): explicit midpoint
     if ((mods & M_ADVECTION) && act) {
       double w0[4], w1[4];
-      sample(a.met, time, lon, lat, p, 7, w0);
+      O::sample(a.met, time, lon, lat, p, 7, w0);
       const double half = 0.5 * dt;
-      const double lon_m = lon + w0[0] * half * kDegPerM / cos_lat(lat);
+      const double lon_m = lon + O::over_cos(w0[0] * half * kDegPerM, lat);
       const double lat_m = lat + w0[1] * half * kDegPerM;
       const double p_m = p + w0[2] * half;
-      sample(a.met, time + half, lon_m, lat_m, p_m, 7, w1);
-      lon = lon + w1[0] * dt * kDegPerM / cos_lat(lat_m);
+      O::sample(a.met, time + half, lon_m, lat_m, p_m, 7, w1);
+      lon = lon + O::over_cos(w1[0] * dt * kDegPerM, lat_m);
       lat = lat + w1[1] * dt * kDegPerM;
       p = p + w1[2] * dt;
       time = time + dt;
@@ -130,16 +168,16 @@ __global__ void __launch_bounds__(256, LT_STEP_MIN_BLOCKS) step_kernel(const Ste
     // post-hop lon/lat and pre-hop p (numpy view aliasing)
     if (want_turb && act) {
       double xt[3];
-      draws(a, s, gid, 1, xt);
+      draws<O>(a, s, gid, 1, xt);
       if (ctl.turb_dx > 0.0) {
         const double sig = sqrt(2.0 * ctl.turb_dx * dt);
-        const double nlon = lon + sig * xt[0] * kDegPerM / cos_lat(lat);
+        const double nlon = lon + O::over_cos(sig * xt[0] * kDegPerM, lat);
         lat = lat + sig * xt[1] * kDegPerM;
         lon = nlon;
       }
       if (ctl.turb_dz > 0.0) {
         double v[4];
-        sample(a.met, time, lon, lat, p, 8, v);
+        O::sample(a.met, time, lon, lat, p, 8, v);
         const double dz = sqrt(2.0 * ctl.turb_dz * dt) * xt[2];
         const double rho = 100.0 * p / (kRAir * v[3]);
         p = p + (-(rho * kG0 * dz) / 100.0);
@@ -149,21 +187,20 @@ __global__ void __launch_bounds__(256, LT_STEP_MIN_BLOCKS) step_kernel(const Ste
     // physics.py:150-188 (module_diffusion_meso): AR(1) with met0 cell spread
     if (want_meso && act) {
       double xm[3];
-      draws(a, s, gid, 2, xm);
-      const Cell c = cell_of(a.met, lon, lat, p);
+      draws<O>(a, s, gid, 2, xm);
       Corners<Rec> q;
-      gather(a.met.s0, a.met, c.r00, q);
+      gather(a.met.s0, a.met, O::cell(a.met, lon, lat, p), q);
       double r = 1.0 - 2.0 * dt / ctl.met_dt;
       r = fmin(fmax(r, 0.0), 1.0);
       const double amp = sqrt(1.0 - r * r);
       double pert[3];
 #pragma unroll
       for (int f = 0; f < 3; ++f) {
-        const double sigma = ctl.turb_meso * corner_std(q, f);
+        const double sigma = ctl.turb_meso * O::spread(q, f);
         pert[f] = r * a.uvwp[f * a.cap + s] + amp * sigma * xm[f];
         a.uvwp[f * a.cap + s] = pert[f];
       }
-      const double nlon = lon + pert[0] * dt * kDegPerM / cos_lat(lat);
+      const double nlon = lon + O::over_cos(pert[0] * dt * kDegPerM, lat);
       lat = lat + pert[1] * dt * kDegPerM;
       lon = nlon;
       p = p + pert[2] * dt;
@@ -172,7 +209,7 @@ __global__ void __launch_bounds__(256, LT_STEP_MIN_BLOCKS) step_kernel(const Ste
     // physics.py:191-203 (module_convection)
     if (want_conv && act) {
       double xc[3];
-      draws(a, s, gid, 0, xc);
+      draws<O>(a, s, gid, 0, xc);
       if (p > ctl.conv_p_top && xc[0] < ctl.conv_prob)
         p = ctl.conv_p_top + (xc[0] / ctl.conv_prob) * (ctl.p_surf - ctl.conv_p_top);
     }
@@ -180,7 +217,7 @@ __global__ void __launch_bounds__(256, LT_STEP_MIN_BLOCKS) step_kernel(const Ste
     // physics.py:206-222 (module_sedi): Stokes settling
     if ((mods & M_SEDI) && ctl.sedi_radius != 0.0 && act) {
       double v[4];
-      sample(a.met, time, lon, lat, p, 8, v);
+      O::sample(a.met, time, lon, lat, p, 8, v);
       const double rho = 100.0 * p / (kRAir * v[3]);
       const double vs = 2.0 * (ctl.sedi_radius * ctl.sedi_radius) * (ctl.sedi_density - rho) *
                         kG0 / (9.0 * kEtaAir);
@@ -203,7 +240,7 @@ __global__ void __launch_bounds__(256, LT_STEP_MIN_BLOCKS) step_kernel(const Ste
         bool pending = true;
         for (int it = 0; it < 10 && pending; ++it) {
           double v[4];
-          sample(a.met, time, lon, lat, p, 8, v);
+          O::sample(a.met, time, lon, lat, p, 8, v);
           const double pn = 1000.0 * pow(v[3] / theta0, kInvKappa);
           const double dp = pn - p;
           p = pn;
@@ -234,7 +271,7 @@ __global__ void __launch_bounds__(256, LT_STEP_MIN_BLOCKS) step_kernel(const Ste
     // physics.py:290-301 (module_meteo): sample T,u,v and climatology
     if (mods & M_METEO) {
       double v[4];
-      sample(a.met, time, lon, lat, p, 11, v);
+      O::sample(a.met, time, lon, lat, p, 11, v);
       a.q[s] = v[3];
       a.q[a.cap + s] = v[0];
       a.q[2 * a.cap + s] = v[1];

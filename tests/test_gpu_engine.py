@@ -159,3 +159,35 @@ def test_met_rotation_matches_oracle(eng):
     e.close()
     for k in ("lon", "lat", "p", "time"):
         np.testing.assert_allclose(getattr(got, k), st[k], rtol=1e-10, atol=1e-9)
+
+
+def _engine_run(engine, m0, m1, ens, ctl, steps, mask, sort_every=0):
+    e = engine.Engine(device=0)
+    e.upload(ens)
+    e.bind_met(m0, m1)
+    for step in range(steps):
+        if sort_every and step % sort_every == 0:
+            e.sort()
+        e.step(ctl, step, mask)
+    out = e.download()
+    e.close()
+    return out
+
+
+def test_fast_precision_within_north_star_tolerance(eng):
+    """precision='fast' (fp32 interpolation arithmetic, fp64 state) stays
+    within the north star's ~1e-5 run tolerance of the exact kernels over a
+    24 h cfg2-style run (1 deg ERA5-like met, adv + turb + meso, 480 steps)."""
+    engine, ms, syn = eng
+    m0, m1 = syn.analytic_pair(1.0, 1.0, 60, 0.0, 10800.0)
+    ens = syn.particles(200_000, seed=21)
+    kw = dict(t_stop=86400.0, dt_model=180.0, met_dt=10800.0, rng_mode="counter",
+              rng_seed_global=5)
+    exact = _engine_run(engine, m0, m1, ens, ms.Control(**kw), 480, engine.ADV_DIFF, 40)
+    fast = _engine_run(engine, m0, m1, ens, ms.Control(precision="fast", **kw), 480,
+                       engine.ADV_DIFF, 40)
+    dlon = np.abs((fast.lon - exact.lon + 180.0) % 360.0 - 180.0)
+    assert dlon.max() / 360.0 <= 1e-5
+    assert np.abs(fast.lat - exact.lat).max() / 180.0 <= 1e-5
+    assert (np.abs(fast.p - exact.p) / exact.p).max() <= 1e-5
+    np.testing.assert_array_equal(fast.time, exact.time)
