@@ -157,7 +157,9 @@ int lt_clim_load(lt_ctx *ctx, int32_t nlat, int32_t np_, const double *lat_grid,
 int lt_run(lt_ctx *ctx, const lt_control *ctl, uint32_t modules, int64_t start,
            int64_t end, int64_t step, uint64_t faithful_state,
            int64_t faithful_base, uint32_t flags);
-/* fill the device RandomBatch for [start, end) (rng.py:156-181) */
+/* fill the device RandomBatch for [start, end) (rng.py:156-181); counter and
+   philox draws are keyed by the slot's global particle id (LT_F_ID) once the
+   store has ids (a shard or a sorted layout), else by the slot index */
 int lt_rng_fill(lt_ctx *ctx, int32_t mode, uint64_t seed_or_state, int64_t step,
                 int64_t start, int64_t end);
 /* interpolate_met (physics.py:69-79) at n host points: out = u,v,w,T rows (4n) */

@@ -165,9 +165,10 @@ class DeviceContext:
     def slot_key(self, slot: int):
         return self._slot_keys[slot]
 
-    def bind_pair(self, met0, met1) -> None:
+    def bind_pair(self, met0, met1) -> tuple[int, int]:
         """Make (met0, met1) the active snapshot pair, uploading only what
-        changed (module-API path; grids must be identical)."""
+        changed (module-API path; grids must be identical).  Returns the
+        (met0, met1) slot numbers."""
         for name in ("lons", "lats", "levs"):
             if not np.array_equal(np.asarray(getattr(met0, name)), np.asarray(getattr(met1, name))):
                 raise ValueError("met0 and met1 must share one grid on the B200 met store")
@@ -189,6 +190,7 @@ class DeviceContext:
             self.load_met(free, met, key)
             slots[key] = free
         self.use_met(slots[k0], slots[k1])
+        return slots[k0], slots[k1]
 
     def load_clim(self, clim) -> None:
         lat, pg = _f64(clim.lat_grid), _f64(clim.p_grid)

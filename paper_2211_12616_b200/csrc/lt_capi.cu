@@ -687,7 +687,7 @@ int lt_rng_fill(lt_ctx* c, int32_t mode, uint64_t seed, int64_t step, int64_t st
                 (long long)start, (long long)end, (long long)c->cap);
   if (mode < 0 || mode > 2) return fail(LT_ERR_ARG, "unknown rng mode %d", mode);
   if (c->timing) CK(cudaEventRecord(c->ev_start, c->stream));
-  CK(launch_rng_fill(mode, seed, step, start, end, c->rnd_conv, c->rnd_turb, c->rnd_meso, c->stream));
+  CK(launch_rng_fill(mode, seed, step, start, end, c->ids, c->rnd_conv, c->rnd_turb, c->rnd_meso, c->stream));
   if (c->timing) { CK(cudaEventRecord(c->ev_stop, c->stream)); c->timed_once = true; }
   return LT_OK;
 }

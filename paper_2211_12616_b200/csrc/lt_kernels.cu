@@ -46,20 +46,25 @@ __global__ void pack_nodes_kernel(Rec* out, const float4* nodes, int nx, int ny,
   }
 }
 
-// rng.py:156-181: fill the RandomBatch of [start, end)
+// rng.py:156-181: fill the RandomBatch of [start, end).  Counter and Philox
+// draws are keyed by the particle's global index: ids[s] when the store
+// holds a shard (or a sorted layout), else the slot s itself.  Faithful
+// draws walk the device stream from the range start (rng.py:105-126).
 __global__ void rng_fill_kernel(int mode, uint64_t seed_or_state, int64_t step, int64_t start,
-                                int64_t end, double* conv, double* turb, double* meso) {
+                                int64_t end, const uint32_t* ids, double* conv, double* turb,
+                                double* meso) {
   for (int64_t s = start + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; s < end;
        s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     double c, t[3], m[3];
+    const uint64_t gid = ids ? static_cast<uint64_t>(ids[s]) : static_cast<uint64_t>(s);
     if (mode == RNG_COUNTER) {
-      c = to_unit(counter_word(seed_or_state, step, static_cast<uint64_t>(s), 0, 0));
-      counter_normals(seed_or_state, step, static_cast<uint64_t>(s), 1, t);
-      counter_normals(seed_or_state, step, static_cast<uint64_t>(s), 2, m);
+      c = to_unit(counter_word(seed_or_state, step, gid, 0, 0));
+      counter_normals(seed_or_state, step, gid, 1, t);
+      counter_normals(seed_or_state, step, gid, 2, m);
     } else if (mode == RNG_FAITHFUL) {
       faithful_draws(seed_or_state, static_cast<uint64_t>(s - start), c, t, m);
     } else {
-      philox_draws(seed_or_state, step, static_cast<uint64_t>(s), c, t, m);
+      philox_draws(seed_or_state, step, gid, c, t, m);
     }
     conv[s] = c;
 #pragma unroll
@@ -172,9 +177,11 @@ template cudaError_t launch_pack_nodes<RecF>(RecF*, const float4*, int, int, int
 template cudaError_t launch_pack_nodes<RecD>(RecD*, const float4*, int, int, int, int, cudaStream_t);
 
 cudaError_t launch_rng_fill(int mode, uint64_t seed, int64_t step, int64_t start, int64_t end,
-                            double* conv, double* turb, double* meso, cudaStream_t st) {
+                            const uint32_t* ids, double* conv, double* turb, double* meso,
+                            cudaStream_t st) {
   if (end <= start) return cudaSuccess;
-  rng_fill_kernel<<<grid_for(end - start), 256, 0, st>>>(mode, seed, step, start, end, conv, turb, meso);
+  rng_fill_kernel<<<grid_for(end - start), 256, 0, st>>>(mode, seed, step, start, end, ids, conv,
+                                                         turb, meso);
   return cudaGetLastError();
 }
 

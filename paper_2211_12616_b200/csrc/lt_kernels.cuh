@@ -24,7 +24,8 @@ template <class Rec>
 cudaError_t launch_pack_nodes(Rec* out, const float4* nodes, int nx, int ny, int nz, int nx_src,
                               cudaStream_t st);
 cudaError_t launch_rng_fill(int mode, uint64_t seed, int64_t step, int64_t start, int64_t end,
-                            double* conv, double* turb, double* meso, cudaStream_t st);
+                            const uint32_t* ids, double* conv, double* turb, double* meso,
+                            cudaStream_t st);
 template <class Rec>
 cudaError_t launch_box_keys(const MetView<Rec>& m, const double* lon, const double* lat,
                             const double* p, int64_t start, int64_t n, uint32_t* keys,

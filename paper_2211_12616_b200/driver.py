@@ -1,0 +1,225 @@
+"""The time loop around the hot path on device-resident GPU images —
+`lagtrans.driver_cli.run_simulation`'s step loop (driver_cli.py:84-209)
+without its file I/O and CLI (out of scope: SURVEY.md §2.1).
+
+Two stepping modes over a `device_runtime.DevicePool`:
+
+* ``fused=False`` — the reference's per-device closure verbatim
+  (driver_cli.py:151-183): module_timesteps, generate_random_nums and the
+  eight physics modules called through the drop-in module API on each
+  device's HBM image, one kernel launch per module.  Each module is timed
+  with CUDA events into the caller's timer sink under the reference names,
+  groups and scopes (the c10 contract, test_acceptance.py:284-305).
+* ``fused=True`` (production) — one launch of the fused step kernel per
+  device per step with in-kernel draws (identical numbers in counter mode),
+  an optional periodic box sort, and met snapshots prefetched into the
+  third met slot on each device's copy stream while steps run.
+
+Met snapshots come from memory (a list of `MeteoField`, already closed with
+`met_periodic`), replacing the text reader `ingest.read_met`; rotation
+follows driver_cli.py:139-149.  Output cadence (driver_cli.py:188-195)
+copies every device's owned range back into the host ensemble and calls
+`on_output(ctl, ens, cache, t)`.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+
+import numpy as np
+
+from . import _capi as capi
+from . import engine as eng
+from . import physics
+from .device_runtime import REGION_FIELDS, DevicePool, DeviceTaskError, ModelImage
+from .model_state import cache_allocate, validate_control
+from .partition import partition_all
+from .rng import batch_allocate, generate_random_nums, module_rng_init
+
+_OUT_EPS = 1e-9  # driver_cli.py:35
+PIPELINE = ("module_advection", "module_diffusion_turb", "module_diffusion_meso",
+            "module_convection", "module_sedi", "module_isosurf", "module_position",
+            "module_meteo")  # driver_cli.py:31-33
+
+
+def device_scope(d: int) -> str:
+    return f"device{d}"
+
+
+class _NullTimers:
+    def record(self, name, group, scope, elapsed_ns):
+        pass
+
+
+def n_steps_for(ctl) -> int:
+    """driver_cli.py:131-132."""
+    return max(0, math.ceil((ctl.t_stop - ctl.t_start) / ctl.dt_model - _OUT_EPS))
+
+
+def bracketing(mets, t_start):
+    """driver_cli.py:67-81 over in-memory snapshots: (met0, met1, rest)."""
+    if not mets:
+        raise ValueError("no met snapshots")
+    met0 = mets[0]
+    rest = list(mets[1:])
+    met1 = rest.pop(0) if rest else met0
+    while met1.t_met < t_start and rest:
+        met0, met1 = met1, rest.pop(0)
+    if met0.t_met > t_start:
+        raise ValueError(f"first met snapshot ({met0.t_met} s) is after t_start ({t_start} s)")
+    return met0, met1, rest
+
+
+def run_simulation(ctl, ens, mets, num_devices: int = 1, *, fused: bool = True,
+                   modules: int | None = None, sort_every: int = 0, clim=None,
+                   timers=None, on_output=None, parallel: bool = True,
+                   device_map=None):
+    """Advance `ens` (host ParticleEnsemble, updated in place at every
+    output time) from ctl.t_start to ctl.t_stop.  Returns (status, cache):
+    status 0 on success, 1 when a device task failed (driver_cli.py:196-199).
+    """
+    violations = validate_control(ctl)
+    if violations:
+        raise ValueError("invalid control: " + "; ".join(violations))
+    timers = timers or _NullTimers()
+    if clim is None:
+        from .model_state import read_clim
+        clim = read_clim(ctl)
+    if modules is None:
+        modules = eng.FULL
+    met0, met1, rest = bracketing(list(mets), ctl.t_start)
+    cache = cache_allocate(ens.np)
+    host = ModelImage(ctl=ctl, ens=ens, cache=cache, clim=clim, met0=met0, met1=met1,
+                      dt=np.zeros(ens.np), batch=batch_allocate(ens.np) if not fused else None)
+    rng = module_rng_init(ctl, num_devices)
+    ranges = partition_all(ens.np, num_devices)
+    pool = DevicePool(num_devices, debug=True, device_map=device_map)
+    regions = []
+    status = 0
+
+    def timed(name, group, scope, fn):
+        t0 = time.perf_counter_ns()
+        fn()
+        timers.record(name, group, scope, time.perf_counter_ns() - t0)
+
+    try:
+        for d in range(num_devices):
+            timed("ACC_INIT", "INIT", device_scope(d),
+                  lambda d=d: pool.dispatch(d, lambda: None).result())
+        fields = tuple(f for f in REGION_FIELDS if not (fused and f == "batch"))
+        for d in range(num_devices):
+            timed("CREATE_DATA_REGION", "MEMORY", device_scope(d),
+                  lambda d=d: regions.append(pool.region_create(d, host, ranges[d],
+                                                                with_batch=not fused)))
+            timed("UPDATE_DEVICE", "MEMORY", device_scope(d),
+                  lambda d=d: pool.region_update_device(regions[d], host, fields))
+
+        def init(d):
+            img = regions[d].image
+            physics.module_isosurf_init(img.ctl, img.ens, met0, met1, img.cache, ranges[d])
+        pool.for_each_device_parallel(init, parallel=parallel)
+
+        # fused mode: the next snapshot is staged into each device's free slot
+        def prefetch(d):
+            if rest:
+                regions[d].image.engine.prefetch(met=rest[0])
+        if fused:
+            pool.for_each_device_parallel(prefetch, parallel=parallel)
+
+        t = ctl.t_start
+        next_out = ctl.t_start + ctl.output_dt
+        for step in range(n_steps_for(ctl)):
+            t_next = min(t + ctl.dt_model, ctl.t_stop)
+            while met1.t_met < t_next:      # driver_cli.py:139-149
+                if not rest:
+                    raise ValueError(f"t_stop {ctl.t_stop} s exceeds the last met snapshot "
+                                     f"time {met1.t_met} s")
+                met0, met1 = met1, rest.pop(0)
+                host.met0, host.met1 = met0, met1
+                for d in range(num_devices):
+                    img = regions[d].image
+                    if fused:
+                        def rot(img=img):
+                            img.engine.rotate()
+                            img.met0, img.met1 = met0, met1
+                        timed("UPDATE_DEVICE", "MEMORY", device_scope(d),
+                              lambda d=d, rot=rot: pool.dispatch(d, rot).result())
+                    else:
+                        timed("UPDATE_DEVICE", "MEMORY", device_scope(d),
+                              lambda d=d: pool.region_update_device(regions[d], host,
+                                                                    ("met0", "met1")))
+                if fused:
+                    pool.for_each_device_parallel(prefetch, parallel=parallel)
+
+            if fused:
+                def device_step(d, step=step):
+                    img = regions[d].image
+                    if sort_every and step % sort_every == 0:
+                        img.engine.sort()
+                    ctx = img.engine.ctx
+                    ctx.timing(True)
+                    img.engine.step(img.ctl, step, modules, device_id=d,
+                                    num_devices=num_devices)
+                    ms = ctx.last_elapsed_ms()
+                    ctx.timing(False)
+                    timers.record("module_fused_step", "PHYSICS", device_scope(d),
+                                  int(ms * 1e6))
+            else:
+                def device_step(d, step=step, t_next=t_next):
+                    _module_step(regions[d].image, ranges[d], d, step, t_next, rng,
+                                 met0, met1, timers)
+            pool.for_each_device_parallel(device_step, parallel=parallel)
+            t = t_next
+
+            if t >= next_out - _OUT_EPS or t >= ctl.t_stop:   # driver_cli.py:188-195
+                for d in range(num_devices):
+                    timed("UPDATE_HOST", "MEMORY", device_scope(d),
+                          lambda d=d: pool.region_update_host(regions[d], host, ranges[d]))
+                if on_output is not None:
+                    on_output(ctl, ens, cache, t)
+                while next_out <= t + _OUT_EPS:
+                    next_out += ctl.output_dt
+    except DeviceTaskError as exc:
+        import sys
+        for d, err in sorted(exc.failures.items()):
+            print(f"device {d} failed: {err!r}", file=sys.stderr)
+        status = 1
+    finally:
+        for region in regions:
+            pool.device_wait(region.device_id)
+            if region.state != "deleted":
+                timed("DELETE_DATA_REGION", "MEMORY", device_scope(region.device_id),
+                      lambda r=region: pool.region_delete(r))
+        pool.shutdown()
+    return status, cache
+
+
+def _module_step(img, work, d, step, t_next, rng, met0, met1, timers):
+    """driver_cli.py:151-183 on one device image, each module CUDA-event timed."""
+    ctx = img.engine.ctx
+    scope = device_scope(d)
+
+    def timed(name, fn):
+        ctx.timing(True)
+        fn()
+        ms = ctx.last_elapsed_ms()
+        ctx.timing(False)
+        timers.record(name, "PHYSICS", scope, int(ms * 1e6))
+
+    c, e = img.ctl, img.ens
+    timed("module_timesteps", lambda: physics.module_timesteps(c, e, t_next, work, img.dt))
+    timed("generate_random_nums", lambda: generate_random_nums(rng, step, work, d, img.batch))
+    timed("module_advection", lambda: physics.module_advection(c, e, met0, met1, img.dt, work))
+    timed("module_diffusion_turb",
+          lambda: physics.module_diffusion_turb(c, e, met0, met1, img.dt, img.batch, work))
+    timed("module_diffusion_meso",
+          lambda: physics.module_diffusion_meso(c, e, met0, met1, img.dt, img.batch, img.cache,
+                                                work))
+    timed("module_convection", lambda: physics.module_convection(c, e, img.dt, img.batch, work))
+    timed("module_sedi", lambda: physics.module_sedi(c, e, met0, met1, img.dt, work))
+    if getattr(c, "decay_tau", 0.0) > 0:
+        timed("module_decay", lambda: physics.module_decay(c, e, img.dt, work))
+    timed("module_isosurf", lambda: physics.module_isosurf(c, e, met0, met1, img.cache, work))
+    timed("module_position", lambda: physics.module_position(c, e, work))
+    timed("module_meteo", lambda: physics.module_meteo(c, e, met0, met1, img.clim, work))

@@ -21,7 +21,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import _capi as capi
-from .context import DeviceContext
+from .context import DeviceContext, met_fingerprint
 from .model_state import ParticleEnsemble
 from .rng import advance_faithful, rng_seed_for
 
@@ -120,19 +120,24 @@ class Engine:
         self._staged = None
         self.ctx.use_met(0, 1)
 
+    def bind_pair(self, met0, met1) -> None:
+        """Select (met0, met1), uploading only snapshots the slots lack."""
+        self._met_slots = self.ctx.bind_pair(met0, met1)
+        self._staged = None
+
     def set_grid(self, lons, lats, levs) -> None:
         self.ctx.set_grid(lons, lats, levs)
 
     def load_slot(self, slot, met=None, nodes=None, t_met=None, close_lon=False) -> None:
         if met is not None:
-            self.ctx.load_met(slot, met, close_lon=close_lon)
+            self.ctx.load_met(slot, met, key=met_fingerprint(met), close_lon=close_lon)
         else:
             self.ctx.load_met_nodes(slot, t_met, nodes, close_lon=close_lon)
 
     def prefetch(self, met=None, nodes=None, t_met=None, close_lon=False) -> None:
         """Stage the next snapshot into the free slot on the copy stream; the
         compute stream keeps stepping on the current pair meanwhile."""
-        free = ({0, 1, 2} - set(self._met_slots)).pop()
+        free = min({0, 1, 2} - set(self._met_slots))
         self.load_slot(free, met=met, nodes=nodes, t_met=t_met, close_lon=close_lon)
         self._staged = free
 

@@ -77,12 +77,19 @@ def advance_faithful(state: int, n: int) -> int:
 def generate_random_nums(rng: RngState, step_index: int, work: WorkRange, device_id: int,
                          batch: RandomBatch) -> None:
     """Fill batch entries of particles in `work` only (rng.py:156-181), on the GPU."""
-    n_total = len(batch.convection)
+    n_total = batch.image.ens.np if getattr(batch, "is_device_resident", False) \
+        else len(batch.convection)
     if not (0 <= work.start <= work.end <= n_total):
         raise IndexError(f"range [{work.start}, {work.end}) outside ensemble of "
                          f"{n_total} particles")
     n = work.size
     if n == 0:
+        return
+    if getattr(batch, "is_device_resident", False):   # a DevicePool image's batch
+        seed = rng.device_states[device_id] if rng.mode == "faithful" else rng.seed_global
+        batch.image.rng_fill(rng.mode, seed, step_index, work)
+        if rng.mode == "faithful":
+            rng.device_states[device_id] = advance_faithful(seed, n)
         return
     from .physics import default_context
     ctx = default_context()

@@ -1,0 +1,162 @@
+"""GPU: the DevicePool mirror (device-resident images behind the module
+API) and the driver loop, against the reference's golden run and against
+each other.  Devices beyond the GPUs present share GPU 0 (device_map)."""
+
+import numpy as np
+import pytest
+
+from conftest import chain_ctl, snapshot_from
+from oracle import lagtrans_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def rt():
+    from paper_2211_12616_b200 import device_runtime, driver, engine, model_state, synthetic
+    return device_runtime, driver, engine, model_state, synthetic
+
+
+def _ens(ms, g, tag):
+    return ms.ParticleEnsemble(np=g[f"{tag}_p"].size, time=g[f"{tag}_time"].copy(),
+                               p=g[f"{tag}_p"].copy(), zeta=g[f"{tag}_zeta"].copy(),
+                               lon=g[f"{tag}_lon"].copy(), lat=g[f"{tag}_lat"].copy(),
+                               q=g[f"{tag}_q"].copy())
+
+
+def _ctl(ms, **kw):
+    base = vars(chain_ctl()).copy()
+    base.update(kw)
+    return ms.Control(**{k: v for k, v in base.items() if k in ms.Control.__dataclass_fields__})
+
+
+@pytest.mark.parametrize("fused,ndev", [(False, 4), (True, 3), (True, 1)])
+def test_driver_matches_reference_golden_chain(rt, golden_chain, fused, ndev):
+    """driver_cli.run_simulation's loop over 1..4 device images reproduces
+    the reference's 50-step all-physics run (acceptance c1 shape)."""
+    _, driver, _, ms, _ = rt
+    g = golden_chain
+    ens = _ens(ms, g, "init")
+    ctl = _ctl(ms, output_dt=1e9)
+    status, cache = driver.run_simulation(ctl, ens, [snapshot_from(g, "m0"), snapshot_from(g, "m1")],
+                                          num_devices=ndev, fused=fused)
+    assert status == 0
+    np.testing.assert_array_equal(ens.time, g["final_time"])
+    for k in ("lon", "lat", "p"):
+        np.testing.assert_allclose(getattr(ens, k), g[f"final_{k}"], rtol=1e-9, atol=1e-9)
+    np.testing.assert_allclose(cache.uvwp, g["final_uvwp"], rtol=1e-9, atol=1e-12)
+
+
+def test_device_count_invariance_bitwise(rt, golden_chain):
+    """Counter mode: 1, 2 and 4 devices give byte-identical states
+    (test_acceptance.py:93-102), fused and module-by-module alike."""
+    _, driver, _, ms, _ = rt
+    g = golden_chain
+    mets = [snapshot_from(g, "m0"), snapshot_from(g, "m1")]
+    ctl = _ctl(ms, output_dt=1e9, t_stop=1800.0)
+    outs = []
+    for fused, nd in ((True, 1), (True, 2), (True, 4), (False, 1), (False, 3)):
+        ens = _ens(ms, g, "init")
+        status, cache = driver.run_simulation(ctl, ens, mets, num_devices=nd, fused=fused,
+                                              sort_every=3 if fused else 0)
+        assert status == 0
+        outs.append(np.stack([ens.lon, ens.lat, ens.p, ens.time, *ens.q, *cache.uvwp]))
+    for o in outs[1:]:
+        np.testing.assert_array_equal(o, outs[0])
+
+
+def test_streamed_met_rotation_matches_oracle(rt):
+    """Snapshots every hour, prefetched into the third met slot while the
+    steps run (fused) vs the oracle stepping with driver_cli's rotation."""
+    _, driver, engine, ms, syn = rt
+    lons, lats, levs = syn.grid(10.0, 5.0, 16)
+    mets = [syn.snapshot(3600.0 * k, lons, lats, levs,
+                         syn.era5_like(lons, lats, levs, 7.0 * k, periodic=True))
+            for k in range(4)]
+    ctl = ms.Control(t_stop=3 * 3600.0, dt_model=600.0, met_dt=3600.0, turb_dx=50.0,
+                     turb_dz=0.1, turb_meso=0.16, sedi_radius=5e-6, sedi_density=2000.0,
+                     decay_tau=7200.0, decay_slot=5, nq=6, rng_mode="counter",
+                     rng_seed_global=99, output_dt=3600.0)
+    ens = syn.particles(3000, seed=5, nq=6)
+    ens.q[5] = 1.0
+    init = {k: getattr(ens, k).copy() for k in ("time", "lon", "lat", "p")}
+    q5 = ens.q[5].copy()
+    seen = []
+    status, _ = driver.run_simulation(ctl, ens, mets, num_devices=2, fused=True,
+                                      modules=engine.modules_mask(
+                                          ("advection", "turb", "meso", "sedi", "decay",
+                                           "position")),
+                                      on_output=lambda c, e, ca, t: seen.append(t))
+    assert status == 0
+    assert seen == [3600.0, 7200.0, 10800.0]
+    st = {"time": init["time"], "lon": init["lon"], "lat": init["lat"], "p": init["p"],
+          "uvwp": np.zeros((3, ens.np)), "iso_var": np.zeros(ens.np), "q": np.zeros((5, ens.np))}
+    snaps = [orc.Snapshot.like(m) for m in mets]
+    t, k = 0.0, 0
+    for step in range(driver.n_steps_for(ctl)):
+        t_next = min(t + ctl.dt_model, ctl.t_stop)
+        while snaps[k + 1].t_met < t_next:
+            k += 1
+        orc.full_step(ctl, snaps[k], snaps[k + 1], st, 0, ens.np, step,
+                      modules=("advection", "turb", "meso", "sedi", "position"))
+        t = t_next
+    for key in ("lon", "lat", "p", "time"):
+        np.testing.assert_allclose(getattr(ens, key), st[key], rtol=1e-9, atol=1e-9)
+    # decay (new module): q *= exp(-dt / tau) per active step
+    np.testing.assert_allclose(ens.q[5], q5 * np.exp(-3 * 3600.0 / 7200.0), rtol=1e-12)
+
+
+def test_lifecycle_errors(rt):
+    dr, _, _, ms, syn = rt
+    from paper_2211_12616_b200._capi import LifecycleError
+    from paper_2211_12616_b200.partition import partition_all
+    ens = syn.particles(100)
+    host = dr.ModelImage(ctl=ms.Control(), ens=ens, cache=ms.cache_allocate(100),
+                         clim=ms.read_clim(), met0=None, met1=None, dt=np.zeros(100), batch=None)
+    ranges = partition_all(100, 2)
+    with dr.DevicePool(2, debug=True) as pool:
+        with pytest.raises(ValueError):
+            pool.dispatch(2, lambda: None)
+        r0 = pool.region_create(0, host, ranges[0])
+        with pytest.raises(LifecycleError):
+            pool.region_create(0, host, ranges[0])
+        with pytest.raises(LifecycleError):
+            pool.region_update_host(r0, host, ranges[0])      # not populated
+        with pytest.raises(ValueError):
+            pool.region_update_device(r0, host, ("bogus",))
+        pool.region_update_device(r0, host, ("ens", "cache"))
+        with pytest.raises(LifecycleError):
+            pool.region_update_host(r0, host, ranges[1])      # not its own range
+        pool.region_update_host(r0, host, ranges[0])
+        np.testing.assert_array_equal(host.ens.lon, ens.lon)
+        pool.region_delete(r0)
+        with pytest.raises(LifecycleError):
+            pool.region_delete(r0)
+        with pytest.raises(dr.DeviceTaskError) as ei:
+            pool.for_each_device_parallel(lambda d: 1 / (d - 1))
+        assert set(ei.value.failures) == {1}
+
+
+def test_module_mode_timer_contract(rt, golden_chain):
+    """Per-module, per-device PHYSICS records (test_acceptance.py:284-305),
+    filled from CUDA events."""
+    _, driver, _, ms, _ = rt
+    g = golden_chain
+    recs = []
+
+    class Sink:
+        def record(self, name, group, scope, ns):
+            recs.append((group, name, scope, ns))
+
+    ctl = _ctl(ms, output_dt=1e9, t_stop=360.0)
+    status, _ = driver.run_simulation(ctl, _ens(ms, g, "init"),
+                                      [snapshot_from(g, "m0"), snapshot_from(g, "m1")],
+                                      num_devices=4, fused=False, timers=Sink())
+    assert status == 0
+    keys = {(gr, n, s) for gr, n, s, _ in recs}
+    for d in range(4):
+        for mod in driver.PIPELINE:
+            assert ("PHYSICS", mod, f"device{d}") in keys
+        assert ("INIT", "ACC_INIT", f"device{d}") in keys
+        assert ("MEMORY", "DELETE_DATA_REGION", f"device{d}") in keys
+    assert all(ns >= 0 for *_, ns in recs)
