@@ -129,33 +129,31 @@ def build_met(wl, rank, ws, torch, dist):
 
 
 def load_met_everywhere(eng, mets, ws, rank, torch, dist):
+    """N = 1: H2D of both snapshots.  N > 1: rank 0's snapshots reach every
+    rank by NCCL broadcast (sharding.broadcast_snapshot) and are packed into
+    the met slots straight from device memory."""
     m0, m1 = mets
     if ws == 1:
         eng.bind_met(m0, m1)
         return m0, m1
     from paper_2211_12616_b200 import _capi as capi
-    from paper_2211_12616_b200.model_state import MeteoField
+    from paper_2211_12616_b200 import sharding
+    dev = torch.device("cuda", torch.cuda.current_device())
     if rank == 0:
         grid = (m0.lons, m0.lats, m0.levs)
-        shape = m0.u.shape
     else:
         lons, lats, levs = m1
         grid = (np.append(lons, lons[0] + 360.0), lats, levs)
-        shape = (len(grid[0]), len(lats), len(levs))
     eng.set_grid(*grid)
-    dev = torch.device("cuda", torch.cuda.current_device())
+    shape = (len(grid[0]), len(grid[1]), len(grid[2]))
     for slot, t_met in ((0, 0.0), (1, 10800.0)):
-        buf = torch.empty((4,) + tuple(shape), dtype=torch.float32, device=dev)
-        if rank == 0:
-            src = (m0, m1)[slot]
-            for f, name in enumerate(("u", "v", "w", "T")):
-                buf[f].copy_(torch.from_numpy(np.ascontiguousarray(getattr(src, name))))
-        dist.broadcast(buf, src=0)
+        src = (m0, m1)[slot] if rank == 0 else None
+        buf = sharding.broadcast_snapshot(src, shape, dist, dev)
         torch.cuda.synchronize()
         p = buf.data_ptr()
         fb = buf[0].numel() * 4
-        eng.ctx.lib.lt_met_load(eng.ctx.h, slot, t_met, 4, p, p + fb, p + 2 * fb, p + 3 * fb,
-                                capi.MET_DEVICE_SRC)
+        capi.check(eng.ctx.lib.lt_met_load(eng.ctx.h, slot, t_met, 4, p, p + fb, p + 2 * fb,
+                                           p + 3 * fb, capi.MET_DEVICE_SRC))
         eng.ctx.sync()
         del buf
     eng.ctx.use_met(0, 1)
@@ -252,6 +250,7 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--precision", default="exact", choices=("exact", "fast"))
+    ap.add_argument("--met-store", default="f32", choices=("f32", "f64"))
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     wl = args.workload
@@ -262,9 +261,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_2211_12616_b200 import engine, synthetic
-    from paper_2211_12616_b200 import _capi as capi
-    from paper_2211_12616_b200.partition import calc_device_workload_range
+    from paper_2211_12616_b200 import engine, sharding, synthetic
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -272,11 +269,11 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     n_tot, dlon, dlat, nlev, pmin, mod, desc = WORKLOADS[wl]
     mask = engine.ADV if mod == "adv" else engine.ADV_DIFF
-    work = calc_device_workload_range(n_tot, ws, rank)
+    work = sharding.shard_range(n_tot, ws, rank)
     ctl = make_ctl(wl, args.precision)
 
     mets = build_met(wl, rank, ws, torch, dist)
-    eng = engine.Engine(device=local, first_id=work.start)
+    eng = engine.Engine(device=local, first_id=work.start, met_precision=args.met_store)
     ens = synthetic.particles(work.size, seed=12616 + rank)
     eng.upload(ens)
     m0, m1 = load_met_everywhere(eng, mets, ws, rank, torch, dist)
@@ -320,43 +317,39 @@ def main():
         barrier()
     total_ms = ev[0].elapsed_time(ev[1])
     kern_ms = [ev[2 + 2 * k].elapsed_time(ev[3 + 2 * k]) for k in range(args.steps)]
-    t = torch.tensor([total_ms, statistics.mean(kern_ms)], device="cuda", dtype=torch.float64)
-    if ws > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms, kern_avg = float(t[0]), float(t[1])
+    total_ms, kern_avg = sharding.max_over_ranks([total_ms, statistics.mean(kern_ms)], dist,
+                                                 "cuda")
     value = n_tot * args.steps / (total_ms / 1e3)
 
-    # e2e: the host-buffer path (pinned SoA in, fused step, SoA out) every step
+    # e2e: the public host-buffer API (Engine.step_host -> lt_run_host): the
+    # shard's SoA sits in pinned host memory; every step streams it through
+    # the GPU (H2D, fused step, D2H overlapped in chunks) and lands back.
     e2e = None
-    fields = [capi.F_TIME, capi.F_P, capi.F_LON, capi.F_LAT]
-    rows = [(f, 0) for f in fields] + ([(capi.F_UVWP, c) for c in range(3)]
-                                       if mod != "adv" else [])
     if args.e2e_steps > 0:
+        from paper_2211_12616_b200 import model_state as ms
+        from paper_2211_12616_b200.context import pinned_empty
         n = work.size
-        host = [torch.empty(n, dtype=torch.float64, pin_memory=True) for _ in rows]
-        for (f, r), h in zip(rows, host):
-            eng.ctx.d2h_ordered(f, r, 0, n, eng.first_id, out=h.numpy())
-        eng.upload(ens)  # unsorted layout: the host path copies particles in order
+        hens = ms.ParticleEnsemble(n, pinned_empty(n), pinned_empty(n), np.zeros(1),
+                                   pinned_empty(n), pinned_empty(n), np.zeros((5, 1)))
+        hcache = ms.CacheState(uvwp=pinned_empty((3, n)), iso_var=np.zeros(1))
+        for k in ("time", "p", "lon", "lat"):
+            getattr(hens, k)[:] = getattr(ens, k)
+        hcache.uvwp[:] = 0.0
+        eng.step_host(ctl, hens, hcache, step, mask)   # warm-up (allocations, events)
+        step += 1
         barrier()
-        t0 = torch.cuda.Event(enable_timing=True)
-        t1 = torch.cuda.Event(enable_timing=True)
-        t0.record(stream)
+        t0 = time.perf_counter()
         for k in range(args.e2e_steps):
-            for (f, r), h in zip(rows, host):
-                eng.ctx.lib.lt_field_h2d(eng.ctx.h, f, r, 0, n, h.data_ptr())
-            eng.step(ctl, step, mask)
+            eng.step_host(ctl, hens, hcache, step, mask)
             step += 1
-            for (f, r), h in zip(rows, host):
-                eng.ctx.lib.lt_field_d2h(eng.ctx.h, f, r, 0, n, h.data_ptr())
-        t1.record(stream)
         barrier()
-        te = torch.tensor([t0.elapsed_time(t1)], device="cuda", dtype=torch.float64)
-        if ws > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        bytes_step = 8 * len(rows) * n_tot
-        e2e = {"value": n_tot * args.e2e_steps / (float(te[0]) / 1e3), "unit": "particle-steps/s",
-               "h2d_bytes_per_step": bytes_step, "d2h_bytes_per_step": bytes_step,
-               "path": "lt_field_h2d (pinned) -> lt_run fused step -> lt_field_d2h, per step"}
+        te = sharding.max_over_ranks([time.perf_counter() - t0], dist, "cuda")[0]
+        rows_in = 4 + (3 if mod != "adv" else 0)
+        rows_out = rows_in
+        e2e = {"value": n_tot * args.e2e_steps / te, "unit": "particle-steps/s",
+               "h2d_bytes_per_step": 8 * rows_in * n_tot, "d2h_bytes_per_step": 8 * rows_out * n_tot,
+               "path": "Engine.step_host -> lt_run_host: pinned host SoA, chunked H2D / fused "
+                       "step / D2H on three streams, every step"}
 
     # roofline of the dominant kernel (step_kernel), algorithmic bytes
     b = algorithmic_bytes(mod, work.size, nodes)
@@ -380,7 +373,7 @@ def main():
                "sample": f"oracle/ numpy port, {n_sample} particles x 2 timed steps on the "
                          f"same {wl} met grid ({wall:.1f} s)"}
 
-    launches = args.steps + n_sorts * 17
+    launches = args.steps + n_sorts * 13  # keys 1 + CUB 6 + row gathers 5 + ids 1
     if rank == 0:
         print(json.dumps({
             "metric": METRIC, "value": value, "unit": "particle-steps/s", "n_gpus": ws,
@@ -389,7 +382,7 @@ def main():
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": wl, "description": desc, "particles": n_tot,
                        "particles_per_gpu": work.size, "met_nodes": nodes,
-                       "met_store": "fp32 node-pair records", "state": "fp64 SoA",
+                       "met_store": f"{args.met_store} node-pair records", "state": "fp64 SoA",
                        "precision": args.precision,
                        "rng": "counter (bit-identical to reference), in-kernel",
                        "sort_every": sort_every, "parallelism": f"particles sharded x{ws}",

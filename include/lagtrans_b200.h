@@ -157,6 +157,26 @@ int lt_clim_load(lt_ctx *ctx, int32_t nlat, int32_t np_, const double *lat_grid,
 int lt_run(lt_ctx *ctx, const lt_control *ctl, uint32_t modules, int64_t start,
            int64_t end, int64_t step, uint64_t faithful_state,
            int64_t faithful_base, uint32_t flags);
+/* host-buffer step (the module API's numpy path, physics.py:82-301 called
+   on host arrays): particles [0, n) live in host memory (pinned for full
+   PCIe overlap).  They stream through the context's particle store in
+   chunks of `chunk` particles: H2D on the copy stream, the fused modules on
+   the compute stream, D2H on a third stream, so both PCIe directions and
+   the kernel overlap.  Particle i has global id first_id + i (RNG key).
+   The store (and its ids) is scratch for the duration of the call; the
+   call returns after every result has landed in host memory. */
+typedef struct lt_host_soa {
+  double *time, *p, *lon, *lat; /* required (read + write) */
+  double *uvwp;                 /* 3 rows of `stride` doubles; LT_MOD_MESO */
+  double *iso_var;              /* LT_MOD_ISOSURF / LT_MOD_ISOSURF_INIT */
+  double *q;                    /* nq rows of `stride` doubles; METEO / DECAY */
+  int64_t stride;               /* row stride of uvwp and q (>= n) */
+  int32_t nq;
+} lt_host_soa;
+int lt_run_host(lt_ctx *ctx, const lt_control *ctl, uint32_t modules, int64_t n,
+                int64_t step, int64_t first_id, uint64_t faithful_state,
+                const lt_host_soa *io, int64_t chunk);
+
 /* fill the device RandomBatch for [start, end) (rng.py:156-181); counter and
    philox draws are keyed by the slot's global particle id (LT_F_ID) once the
    store has ids (a shard or a sorted layout), else by the slot index */

@@ -67,6 +67,13 @@ class LtControl(C.Structure):
                 ("precision", C.c_int32)]
 
 
+class LtHostSoa(C.Structure):
+    """lt_host_soa: host particle rows for lt_run_host."""
+    _fields_ = [("time", C.c_void_p), ("p", C.c_void_p), ("lon", C.c_void_p),
+                ("lat", C.c_void_p), ("uvwp", C.c_void_p), ("iso_var", C.c_void_p),
+                ("q", C.c_void_p), ("stride", C.c_int64), ("nq", C.c_int32)]
+
+
 def control_struct(ctl) -> LtControl:
     """Pack any Control-like object (reference or mirror) into lt_control."""
     iso = ctl.isosurf_mode
@@ -118,6 +125,8 @@ _PROTOS = {
     "lt_host_alloc": ([_I64, C.POINTER(_P)], C.c_int),
     "lt_host_free": ([_P], C.c_int),
     "lt_interpolate": ([_P, _I64, _P, _P, _P, _P, _P], C.c_int),
+    "lt_run_host": ([_P, C.POINTER(LtControl), _U32, _I64, _I64, _I64, _U64,
+                     C.POINTER(LtHostSoa), _I64], C.c_int),
 }
 EXPORTED = tuple(_PROTOS)
 

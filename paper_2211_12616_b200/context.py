@@ -34,6 +34,22 @@ def met_fingerprint(met) -> tuple:
     return (float(met.t_met), h.hexdigest())
 
 
+def pinned_empty(shape, dtype=np.float64) -> np.ndarray:
+    """A numpy array in page-locked host memory (cudaHostAlloc), freed when
+    the array is garbage collected; host-path copies from it run at full
+    PCIe rate and overlap the kernels."""
+    import weakref
+    lib = capi.load()
+    count = int(np.prod(shape))
+    nbytes = max(count * np.dtype(dtype).itemsize, 8)
+    p = C.c_void_p()
+    capi.check(lib.lt_host_alloc(nbytes, C.byref(p)))
+    buf = (C.c_char * nbytes).from_address(p.value)
+    arr = np.frombuffer(buf, dtype=dtype, count=count).reshape(shape)
+    weakref.finalize(buf, lib.lt_host_free, C.c_void_p(p.value))
+    return arr
+
+
 class DeviceContext:
     """Owns one lt_ctx on `device`; all methods raise the reference's
     exception types on failure (ValueError, IndexError, LifecycleError)."""
@@ -208,6 +224,28 @@ class DeviceContext:
         c = ctl if isinstance(ctl, capi.LtControl) else capi.control_struct(ctl)
         capi.check(self.lib.lt_run(self.h, C.byref(c), modules, start, end, step,
                                    faithful_state & 0xFFFFFFFFFFFFFFFF, faithful_base, flags))
+
+    def run_host(self, ctl, modules: int, n: int, step: int, first_id: int, time, p, lon, lat,
+                 uvwp=None, iso_var=None, q=None, faithful_state: int = 0,
+                 chunk: int = 0) -> None:
+        """lt_run_host on C-contiguous float64 host arrays (updated in place)."""
+        c = ctl if isinstance(ctl, capi.LtControl) else capi.control_struct(ctl)
+        arrs = [time, p, lon, lat]
+        for a in arrs + [x for x in (uvwp, iso_var, q) if x is not None]:
+            if a.dtype != np.float64 or not a.flags.c_contiguous or not a.flags.writeable:
+                raise ValueError("host rows must be writeable C-contiguous float64 arrays")
+        rows2 = [x for x in (uvwp, q) if x is not None]
+        stride = rows2[0].shape[1] if rows2 else n
+        if any(x.shape[1] != stride for x in rows2):
+            raise ValueError("uvwp and q must share one row stride")
+        io = capi.LtHostSoa(*[capi.ptr(a) for a in arrs],
+                            capi.ptr(uvwp) if uvwp is not None else None,
+                            capi.ptr(iso_var) if iso_var is not None else None,
+                            capi.ptr(q) if q is not None else None, stride,
+                            q.shape[0] if q is not None else 0)
+        capi.check(self.lib.lt_run_host(self.h, C.byref(c), modules, n, step, first_id,
+                                        faithful_state & 0xFFFFFFFFFFFFFFFF, C.byref(io),
+                                        chunk))
 
     def rng_fill(self, mode: int, seed: int, step: int, start: int, end: int) -> None:
         capi.check(self.lib.lt_rng_fill(self.h, mode, seed & 0xFFFFFFFFFFFFFFFF, step, start, end))

@@ -9,6 +9,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -60,7 +61,9 @@ struct Slot {
 struct lt_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;  // compute
-  cudaStream_t copy = nullptr;    // met streaming
+  cudaStream_t copy = nullptr;    // met streaming, host-path H2D
+  cudaStream_t d2h = nullptr;     // host-path D2H
+  std::vector<cudaEvent_t> ring_ev;  // host-path chunk events (3 per ring slot)
   cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
   cudaEvent_t compute_mark = nullptr;  // last compute-stream work touching met slots
   bool marked = false;
@@ -71,10 +74,12 @@ struct lt_ctx {
   int64_t cap = 0;
   int32_t nq = 0;
   double *time = nullptr, *p = nullptr, *zeta = nullptr, *lon = nullptr, *lat = nullptr;
-  double *q = nullptr, *uvwp = nullptr, *iso_var = nullptr, *dt = nullptr;
+  double *q = nullptr, *iso_var = nullptr, *dt = nullptr;
+  double* uvwp[3] = {nullptr, nullptr, nullptr};  // separate rows: the sort swaps row pointers
   double *rnd_conv = nullptr, *rnd_turb = nullptr, *rnd_meso = nullptr;
   uint32_t* ids = nullptr;
-  double* scratch = nullptr;     // cap doubles (ordered copies, permutation)
+  double* scratch = nullptr;     // cap doubles (ordered copies)
+  double* pool[kRowSet] = {};    // cap doubles each: sort gather targets (swapped with rows)
   uint32_t* sort_buf = nullptr;  // 4 * cap (keys in/out, vals in/out)
   void* cub_temp = nullptr;
   size_t cub_bytes = 0;
@@ -203,7 +208,7 @@ double* field_ptr(lt_ctx* c, int field, int row, int64_t* len, int* rc) {
       return c->q + static_cast<int64_t>(row) * c->cap;
     case LT_F_UVWP:
       if (row < 0 || row >= 3) { *rc = fail(LT_ERR_ARG, "uvwp row %d outside [0, 3)", row); return nullptr; }
-      return c->uvwp + static_cast<int64_t>(row) * c->cap;
+      return c->uvwp[row];
     case LT_F_ISO_VAR: return c->iso_var;
     case LT_F_DT: return c->dt;
     case LT_F_RND_CONV:
@@ -233,6 +238,13 @@ int check_particles(lt_ctx* c) {
 int ensure_scratch(lt_ctx* c) {
   if (!c->scratch)
     return alloc_dev(reinterpret_cast<void**>(&c->scratch), sizeof(double) * c->cap, "scratch");
+  return LT_OK;
+}
+
+int ensure_pool(lt_ctx* c) {
+  for (double*& r : c->pool)
+    if (!r)
+      if (int rc = alloc_dev(reinterpret_cast<void**>(&r), sizeof(double) * c->cap, "sort pool")) return rc;
   return LT_OK;
 }
 
@@ -274,6 +286,7 @@ int lt_ctx_create(int32_t device, lt_ctx** out) {
   c->device = device;
   CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
   CK(cudaEventCreate(&c->ev_start));
   CK(cudaEventCreate(&c->ev_stop));
   CK(cudaEventCreateWithFlags(&c->staging_free, cudaEventDisableTiming));
@@ -291,12 +304,13 @@ int lt_ctx_create(int32_t device, lt_ctx** out) {
 }
 
 static void free_particles(lt_ctx* c) {
-  for (double** p : {&c->time, &c->p, &c->zeta, &c->lon, &c->lat, &c->q, &c->uvwp, &c->iso_var,
+  for (double** p : {&c->time, &c->p, &c->zeta, &c->lon, &c->lat, &c->q, &c->uvwp[0], &c->uvwp[1], &c->uvwp[2], &c->iso_var,
                      &c->dt, &c->rnd_conv, &c->rnd_turb, &c->rnd_meso, &c->scratch}) {
     free_dev(*p);
     *p = nullptr;
   }
   free_dev(c->ids); c->ids = nullptr;
+  for (double*& r : c->pool) { free_dev(r); r = nullptr; }
   free_dev(c->sort_buf); c->sort_buf = nullptr;
   free_dev(c->cub_temp); c->cub_temp = nullptr; c->cub_bytes = 0;
   c->cap = 0;
@@ -307,6 +321,7 @@ int lt_ctx_destroy(lt_ctx* c) {
   if (rc) return rc;
   cudaError_t e1 = cudaStreamSynchronize(c->stream);
   cudaError_t e2 = cudaStreamSynchronize(c->copy);
+  if (e2 == cudaSuccess) e2 = cudaStreamSynchronize(c->d2h);
   free_particles(c);
   for (auto& s : c->slots) {
     free_dev(s.rec);
@@ -327,6 +342,8 @@ int lt_ctx_destroy(lt_ctx* c) {
   cudaEventDestroy(c->compute_mark);
   cudaStreamDestroy(c->stream);
   cudaStreamDestroy(c->copy);
+  cudaStreamDestroy(c->d2h);
+  for (cudaEvent_t e : c->ring_ev) cudaEventDestroy(e);
   delete c;
   if (e1 != cudaSuccess || e2 != cudaSuccess)
     return fail(LT_ERR_CUDA, "pending work failed before destroy: %s",
@@ -338,6 +355,7 @@ int lt_sync(lt_ctx* c) {
   int rc = check_ctx(c);
   if (rc) return rc;
   CK(cudaStreamSynchronize(c->copy));
+  CK(cudaStreamSynchronize(c->d2h));
   CK(cudaStreamSynchronize(c->stream));
   return LT_OK;
 }
@@ -361,7 +379,8 @@ int lt_particles_alloc(lt_ctx* c, int64_t capacity, int32_t nq, int32_t with_bat
   const size_t b = sizeof(double) * static_cast<size_t>(capacity);
   struct { double** p; size_t mult; const char* name; } plan[] = {
       {&c->time, 1, "time"}, {&c->p, 1, "p"}, {&c->zeta, 1, "zeta"}, {&c->lon, 1, "lon"},
-      {&c->lat, 1, "lat"}, {&c->q, static_cast<size_t>(nq), "q"}, {&c->uvwp, 3, "uvwp"},
+      {&c->lat, 1, "lat"}, {&c->q, static_cast<size_t>(nq), "q"}, {&c->uvwp[0], 1, "uvwp"},
+      {&c->uvwp[1], 1, "uvwp"}, {&c->uvwp[2], 1, "uvwp"},
       {&c->iso_var, 1, "iso_var"}, {&c->dt, 1, "dt"}};
   for (auto& e : plan) {
     rc = alloc_dev(reinterpret_cast<void**>(e.p), b * e.mult, e.name);
@@ -620,7 +639,8 @@ static int run_typed(lt_ctx* c, const lt_control* ctl, uint32_t modules, int64_t
                      int64_t end, int64_t step, uint64_t fstate, int64_t fbase, uint32_t flags) {
   StepArgs<Rec> a;
   a.time = c->time; a.p = c->p; a.lon = c->lon; a.lat = c->lat; a.dt = c->dt;
-  a.uvwp = c->uvwp; a.iso_var = c->iso_var; a.q = c->q;
+  for (int k = 0; k < 3; ++k) a.uvwp[k] = c->uvwp[k];
+  a.iso_var = c->iso_var; a.q = c->q;
   a.ids = c->ids;
   a.rnd_conv = c->rnd_conv; a.rnd_turb = c->rnd_turb; a.rnd_meso = c->rnd_meso;
   a.cap = c->cap; a.start = start; a.end = end; a.nq = c->nq;
@@ -675,6 +695,97 @@ int lt_run(lt_ctx* c, const lt_control* ctl, uint32_t modules, int64_t start, in
     CK(cudaEventRecord(c->ev_stop, c->stream));
     c->timed_once = true;
   }
+  return LT_OK;
+}
+
+// Chunked host-buffer step: H2D (copy stream) -> fused step (compute
+// stream) -> D2H (d2h stream), one ring slot per chunk in the particle
+// store.  Events order each slot's three stages and keep a slot from being
+// refilled before its results have been copied out.
+int lt_run_host(lt_ctx* c, const lt_control* ctl, uint32_t modules, int64_t n, int64_t step,
+                int64_t first_id, uint64_t fstate, const lt_host_soa* io, int64_t chunk) {
+  int rc = check_ctx(c);
+  if (rc || (rc = check_particles(c))) return rc;
+  if (!io || !io->time || !io->p || !io->lon || !io->lat)
+    return fail(LT_ERR_ARG, "host SoA needs time, p, lon and lat");
+  if (n < 0) return fail(LT_ERR_ARG, "negative particle count");
+  if (first_id < 0 || first_id + n > (int64_t(1) << 32))
+    return fail(LT_ERR_ARG, "particle ids must fit in 32 bits");
+  const bool meso = modules & M_MESO;
+  const bool iso_in = modules & M_ISOSURF, iso_out = modules & M_ISOSURF_INIT;
+  const bool meteo = modules & M_METEO;
+  const bool decay = (modules & M_DECAY) && ctl->decay_slot >= 0;
+  if (meso && !io->uvwp) return fail(LT_ERR_ARG, "meso needs the uvwp rows");
+  if ((iso_in || iso_out) && !io->iso_var) return fail(LT_ERR_ARG, "isosurf needs iso_var");
+  if ((meteo || decay) && !io->q) return fail(LT_ERR_ARG, "meteo/decay need the q rows");
+  if ((meso || meteo || decay) && io->stride < n) return fail(LT_ERR_ARG, "row stride < n");
+  if (meteo && (io->nq < 5 || c->nq < 5)) return fail(LT_ERR_ARG, "meteo needs 5 q rows");
+  if (decay && (ctl->decay_slot >= io->nq || ctl->decay_slot >= c->nq))
+    return fail(LT_ERR_ARG, "decay_slot outside the q rows");
+  if (n == 0) return LT_OK;
+  if (chunk <= 0) chunk = std::min<int64_t>(c->cap, std::max<int64_t>(int64_t(1) << 20, (n + 15) / 16));
+  chunk = std::min(chunk, c->cap);
+  if (chunk <= 0) return fail(LT_ERR_STATE, "particle store has no capacity");
+  const int64_t nchunks = (n + chunk - 1) / chunk;
+  const int nbuf = static_cast<int>(std::min<int64_t>({nchunks, c->cap / chunk, 32}));
+  if ((rc = ensure_ids(c))) return rc;
+  while (c->ring_ev.size() < static_cast<size_t>(3 * nbuf)) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->ring_ev.push_back(e);
+  }
+  // rows: (device row, host row, copy in, copy out)
+  struct Row { double* dev; double* host; bool in, out; };
+  std::vector<Row> rows;
+  const bool moves = modules & (M_ADVECTION | M_TURB | M_MESO | M_CONVECTION | M_SEDI | M_ISOSURF |
+                                M_POSITION);
+  rows.push_back({c->time, io->time, true, (modules & M_ADVECTION) != 0});
+  rows.push_back({c->p, io->p, true, moves});
+  rows.push_back({c->lon, io->lon, true, moves});
+  rows.push_back({c->lat, io->lat, true, moves});
+  if (meso)
+    for (int k = 0; k < 3; ++k) rows.push_back({c->uvwp[k], io->uvwp + k * io->stride, true, true});
+  if (iso_in || iso_out) rows.push_back({c->iso_var, io->iso_var, iso_in, iso_out});
+  if (meteo)
+    for (int k = 0; k < 5; ++k) rows.push_back({c->q + k * c->cap, io->q + k * io->stride, false, true});
+  if (decay && !(meteo && ctl->decay_slot < 5))
+    rows.push_back({c->q + ctl->decay_slot * c->cap, io->q + ctl->decay_slot * io->stride, true, true});
+  else if (decay)
+    rows[rows.size() - 5 + ctl->decay_slot].in = true;
+  if (c->timing) CK(cudaEventRecord(c->ev_start, c->stream));
+  // the copy stream must not overwrite slots the compute stream still reads
+  CK(cudaEventRecord(c->compute_mark, c->stream));
+  CK(cudaStreamWaitEvent(c->copy, c->compute_mark, 0));
+  for (int64_t k = 0; k < nchunks; ++k) {
+    const int b = static_cast<int>(k % nbuf);
+    const int64_t off = b * chunk, lo = k * chunk, cnt = std::min(chunk, n - lo);
+    cudaEvent_t h2d_done = c->ring_ev[3 * b], run_done = c->ring_ev[3 * b + 1],
+                d2h_done = c->ring_ev[3 * b + 2];
+    if (k >= nbuf) CK(cudaStreamWaitEvent(c->copy, d2h_done, 0));
+    for (const Row& r : rows)
+      if (r.in) CK(cudaMemcpyAsync(r.dev + off, r.host + lo, sizeof(double) * cnt, cudaMemcpyHostToDevice, c->copy));
+    CK(cudaEventRecord(h2d_done, c->copy));
+    CK(cudaStreamWaitEvent(c->stream, h2d_done, 0));
+    CK(launch_iota(c->ids, off, cnt, first_id + lo, c->stream));
+    rc = c->prec == LT_MET_F64
+             ? run_typed<RecD>(c, ctl, modules, off, off + cnt, step, fstate, first_id, LT_RUN_RNG_INKERNEL)
+             : run_typed<RecF>(c, ctl, modules, off, off + cnt, step, fstate, first_id, LT_RUN_RNG_INKERNEL);
+    if (rc) return rc;
+    CK(cudaEventRecord(run_done, c->stream));
+    CK(cudaStreamWaitEvent(c->d2h, run_done, 0));
+    for (const Row& r : rows)
+      if (r.out) CK(cudaMemcpyAsync(r.host + lo, r.dev + off, sizeof(double) * cnt, cudaMemcpyDeviceToHost, c->d2h));
+    CK(cudaEventRecord(d2h_done, c->d2h));
+  }
+  CK(cudaEventRecord(c->compute_mark, c->stream));
+  c->marked = true;
+  if (c->timing) {
+    CK(cudaStreamWaitEvent(c->stream, c->ring_ev[3 * ((nchunks - 1) % nbuf) + 2], 0));
+    CK(cudaEventRecord(c->ev_stop, c->stream));
+    c->timed_once = true;
+  }
+  CK(cudaStreamSynchronize(c->d2h));
+  CK(cudaStreamSynchronize(c->stream));
   return LT_OK;
 }
 
@@ -759,22 +870,31 @@ static int sort_typed(lt_ctx* c, int64_t start, int64_t end) {
   }
   size_t have = c->cub_bytes;
   CK(sort_pairs(c->cub_temp, have, keys_in, keys_out, vals_in, vals_out, n, bits, c->stream));
-  // permute every per-particle row through the scratch row, swapping pointers
-  std::vector<double**> rows = {&c->time, &c->p, &c->zeta, &c->lon, &c->lat, &c->iso_var, &c->dt};
-  double* scratch = c->scratch;
-  for (double** r : rows) {
-    CK(launch_permute<double>(scratch, *r, vals_out, start, n, c->stream));
-    CK(cudaMemcpyAsync(*r + start, scratch + start, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+  // Permute every per-particle row, kRowSet rows per launch into the pool
+  // rows.  Separately allocated rows covering the whole store swap pointers
+  // with their pool row (no copy back); the q block and partial ranges copy
+  // the gathered slice back.
+  if (int rc = ensure_pool(c)) return rc;
+  const bool whole = start == 0 && end == c->cap;
+  std::vector<double**> rows = {&c->time, &c->p, &c->zeta, &c->lon, &c->lat, &c->iso_var, &c->dt,
+                                &c->uvwp[0], &c->uvwp[1], &c->uvwp[2]};
+  for (size_t g = 0; g < rows.size(); g += kRowSet) {
+    RowSet rs;
+    rs.n = static_cast<int>(std::min<size_t>(kRowSet, rows.size() - g));
+    for (int k = 0; k < rs.n; ++k) { rs.src[k] = *rows[g + k]; rs.dst[k] = c->pool[k]; }
+    CK(launch_permute_rows(rs, vals_out, start, n, c->stream));
+    for (int k = 0; k < rs.n; ++k) {
+      if (whole) std::swap(*rows[g + k], c->pool[k]);
+      else CK(cudaMemcpyAsync(*rows[g + k] + start, c->pool[k] + start, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+    }
   }
-  for (int k = 0; k < c->nq; ++k) {
-    double* r = c->q + static_cast<int64_t>(k) * c->cap;
-    CK(launch_permute<double>(scratch, r, vals_out, start, n, c->stream));
-    CK(cudaMemcpyAsync(r + start, scratch + start, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
-  }
-  for (int k = 0; k < 3; ++k) {
-    double* r = c->uvwp + static_cast<int64_t>(k) * c->cap;
-    CK(launch_permute<double>(scratch, r, vals_out, start, n, c->stream));
-    CK(cudaMemcpyAsync(r + start, scratch + start, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+  for (int g = 0; g < c->nq; g += kRowSet) {
+    RowSet rs;
+    rs.n = std::min(kRowSet, c->nq - g);
+    for (int k = 0; k < rs.n; ++k) { rs.src[k] = c->q + static_cast<int64_t>(g + k) * c->cap; rs.dst[k] = c->pool[k]; }
+    CK(launch_permute_rows(rs, vals_out, start, n, c->stream));
+    for (int k = 0; k < rs.n; ++k)
+      CK(cudaMemcpyAsync(c->q + static_cast<int64_t>(g + k) * c->cap + start, c->pool[k] + start, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
   }
   CK(launch_permute<uint32_t>(keys_in, c->ids, vals_out, start, n, c->stream));
   CK(cudaMemcpyAsync(c->ids + start, keys_in + start, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, c->stream));

@@ -96,6 +96,21 @@ __global__ void permute_kernel(T* dst, const T* src, const uint32_t* perm, int64
     dst[start + t] = src[start + perm[t]];
 }
 
+// gather up to kRowSet rows through one permutation (perm read once per particle)
+__global__ void permute_rows_kernel(RowSet r, const uint32_t* perm, int64_t start, int64_t n) {
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t from = start + perm[t];
+    double v[kRowSet];
+#pragma unroll
+    for (int k = 0; k < kRowSet; ++k)
+      if (k < r.n) v[k] = __ldg(r.src[k] + from);
+#pragma unroll
+    for (int k = 0; k < kRowSet; ++k)
+      if (k < r.n) r.dst[k][start + t] = v[k];
+  }
+}
+
 // scatter a sorted slice into original order: out[id - first] = in[s]
 template <class T>
 __global__ void unsort_kernel(T* out, const T* in, const uint32_t* ids, int64_t offset,
@@ -203,6 +218,13 @@ cudaError_t launch_permute(T* dst, const T* src, const uint32_t* perm, int64_t s
 }
 template cudaError_t launch_permute<double>(double*, const double*, const uint32_t*, int64_t, int64_t, cudaStream_t);
 template cudaError_t launch_permute<uint32_t>(uint32_t*, const uint32_t*, const uint32_t*, int64_t, int64_t, cudaStream_t);
+
+cudaError_t launch_permute_rows(const RowSet& r, const uint32_t* perm, int64_t start, int64_t n,
+                               cudaStream_t st) {
+  if (n <= 0 || r.n <= 0) return cudaSuccess;
+  permute_rows_kernel<<<grid_for(n), 256, 0, st>>>(r, perm, start, n);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_unsort(double* out, const double* in, const uint32_t* ids, int64_t offset,
                           int64_t count, int64_t first_id, int* bad, int stride, cudaStream_t st) {

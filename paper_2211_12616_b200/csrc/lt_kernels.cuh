@@ -30,6 +30,14 @@ template <class Rec>
 cudaError_t launch_box_keys(const MetView<Rec>& m, const double* lon, const double* lat,
                             const double* p, int64_t start, int64_t n, uint32_t* keys,
                             uint32_t* vals, cudaStream_t st);
+constexpr int kRowSet = 4;
+struct RowSet {
+  const double* src[kRowSet];
+  double* dst[kRowSet];
+  int n;
+};
+cudaError_t launch_permute_rows(const RowSet& r, const uint32_t* perm, int64_t start, int64_t n,
+                               cudaStream_t st);
 template <class T>
 cudaError_t launch_permute(T* dst, const T* src, const uint32_t* perm, int64_t start, int64_t n,
                            cudaStream_t st);

@@ -9,7 +9,7 @@ namespace lt {
 constexpr uint32_t kChainAdv = M_TIMESTEPS | M_ADVECTION | M_POSITION;
 constexpr uint32_t kChainAdvDiff = M_TIMESTEPS | M_ADVECTION | M_TURB | M_MESO | M_POSITION;
 
-template <class Rec, uint32_t FIXED, bool FAST>
+template <class Rec, uint32_t FIXED, bool FAST, int RM>
 static cudaError_t launch_fixed(const StepArgs<Rec>& a, cudaStream_t st) {
   static int blocks_per_sm = 0;
   static int sms = 0;
@@ -17,7 +17,7 @@ static cudaError_t launch_fixed(const StepArgs<Rec>& a, cudaStream_t st) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, step_kernel<Rec, FIXED, FAST>, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, step_kernel<Rec, FIXED, FAST, RM>, 256, 0);
     if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
   const int64_t n = a.end - a.start;
@@ -25,15 +25,20 @@ static cudaError_t launch_fixed(const StepArgs<Rec>& a, cudaStream_t st) {
   int64_t grid = (n + 255) / 256;
   const int64_t cap = static_cast<int64_t>(sms) * blocks_per_sm * 16;
   if (grid > cap) grid = cap;
-  step_kernel<Rec, FIXED, FAST><<<static_cast<unsigned>(grid), 256, 0, st>>>(a);
+  step_kernel<Rec, FIXED, FAST, RM><<<static_cast<unsigned>(grid), 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 
 template <class Rec, bool FAST>
 static cudaError_t launch_prec(const StepArgs<Rec>& a, cudaStream_t st) {
-  if (a.modules == kChainAdvDiff) return launch_fixed<Rec, kChainAdvDiff, FAST>(a, st);
-  if (a.modules == kChainAdv) return launch_fixed<Rec, kChainAdv, FAST>(a, st);
-  return launch_fixed<Rec, 0, FAST>(a, st);
+  // the production chain gets its in-kernel generator fixed at compile time
+  if (a.modules == kChainAdvDiff && (a.flags & F_RNG_INKERNEL)) {
+    if (a.ctl.rng_mode == RNG_COUNTER) return launch_fixed<Rec, kChainAdvDiff, FAST, RNG_COUNTER>(a, st);
+    if (a.ctl.rng_mode == RNG_PHILOX) return launch_fixed<Rec, kChainAdvDiff, FAST, RNG_PHILOX>(a, st);
+  }
+  if (a.modules == kChainAdvDiff) return launch_fixed<Rec, kChainAdvDiff, FAST, -1>(a, st);
+  if (a.modules == kChainAdv) return launch_fixed<Rec, kChainAdv, FAST, -1>(a, st);
+  return launch_fixed<Rec, 0, FAST, -1>(a, st);
 }
 
 template <class Rec>

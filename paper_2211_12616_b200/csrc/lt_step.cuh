@@ -21,7 +21,7 @@ struct StepArgs {
   double* lon;
   double* lat;
   double* dt;
-  double* uvwp;
+  double* uvwp[3];  // AR(1) mesoscale perturbations (CacheState.uvwp rows)
   double* iso_var;
   double* q;
   const uint32_t* ids;  // global particle index per slot, or null (= slot)
@@ -83,9 +83,21 @@ struct Ops<RecF, true> {
 
 // Draws of one stream for particle slot s / global id gid: stream 0 = the
 // convection uniform (x[0]), 1 = turbulent normals, 2 = mesoscale normals.
-template <class O, class Rec>
+// RM >= 0 fixes the in-kernel generator at compile time (RNG_COUNTER or
+// RNG_PHILOX, no batch); RM = -1 decides at run time.
+template <class O, int RM, class Rec>
 __device__ __forceinline__ void draws(const StepArgs<Rec>& a, int64_t s, uint64_t gid, int stream,
                                       double x[3]) {
+  const Control& ctl = a.ctl;
+  if (RM == RNG_COUNTER) {
+    if (stream == 0) x[0] = to_unit(counter_word(ctl.rng_seed_global, a.step, gid, 0, 0));
+    else O::normals(ctl.rng_seed_global, a.step, gid, stream, x);
+    return;
+  }
+  if (RM == RNG_PHILOX) {
+    philox_stream(ctl.rng_seed_global, a.step, gid, stream, x);
+    return;
+  }
   if (!(a.flags & F_RNG_INKERNEL)) {  // the caller's RandomBatch
     if (stream == 0) {
       x[0] = a.rnd_conv[s];
@@ -95,7 +107,6 @@ __device__ __forceinline__ void draws(const StepArgs<Rec>& a, int64_t s, uint64_
     }
     return;
   }
-  const Control& ctl = a.ctl;
   if (ctl.rng_mode == RNG_COUNTER) {
     if (stream == 0) x[0] = to_unit(counter_word(ctl.rng_seed_global, a.step, gid, 0, 0));
     else O::normals(ctl.rng_seed_global, a.step, gid, stream, x);
@@ -106,7 +117,7 @@ __device__ __forceinline__ void draws(const StepArgs<Rec>& a, int64_t s, uint64_
   }
 }
 
-template <class Rec, uint32_t FIXED, bool FAST>
+template <class Rec, uint32_t FIXED, bool FAST, int RM>
 __global__ void __launch_bounds__(256, LT_STEP_MIN_BLOCKS) step_kernel(const StepArgs<Rec> a) {
   using O = Ops<Rec, FAST>;
   const uint32_t mods = FIXED ? FIXED : a.modules;
@@ -134,7 +145,7 @@ __global__ void __launch_bounds__(256, LT_STEP_MIN_BLOCKS) step_kernel(const Ste
     const bool want_turb = (mods & M_TURB) && (ctl.turb_dx != 0.0 || ctl.turb_dz != 0.0);
     const bool want_meso = (mods & M_MESO) && ctl.turb_meso != 0.0;
     const bool want_conv = (mods & M_CONVECTION) && ctl.conv_prob != 0.0;
-    const uint64_t gid = (a.flags & F_RNG_INKERNEL) && (want_turb || want_meso || want_conv)
+    const uint64_t gid = (RM >= 0 || (a.flags & F_RNG_INKERNEL)) && (want_turb || want_meso || want_conv)
                              ? (a.ids ? static_cast<uint64_t>(a.ids[s]) : static_cast<uint64_t>(s))
                              : 0ull;
 
@@ -149,18 +160,25 @@ __global__ void __launch_bounds__(256, LT_STEP_MIN_BLOCKS) step_kernel(const Ste
       }
     }
 
-    // physics.py:91-116 (module_advection): explicit midpoint
+    // physics.py:91-116 (module_advection): explicit midpoint.  The two
+    // stages share one (rolled) sample call site to keep the kernel small.
     if ((mods & M_ADVECTION) && act) {
-      double w0[4], w1[4];
-      O::sample(a.met, time, lon, lat, p, 7, w0);
       const double half = 0.5 * dt;
-      const double lon_m = lon + O::over_cos(w0[0] * half * kDegPerM, lat);
-      const double lat_m = lat + w0[1] * half * kDegPerM;
-      const double p_m = p + w0[2] * half;
-      O::sample(a.met, time + half, lon_m, lat_m, p_m, 7, w1);
-      lon = lon + O::over_cos(w1[0] * dt * kDegPerM, lat_m);
-      lat = lat + w1[1] * dt * kDegPerM;
-      p = p + w1[2] * dt;
+      double ts = time, xs = lon, ys = lat, zs = p, h = half;
+#pragma unroll 1
+      for (int stage = 0; stage < 2; ++stage) {
+        double w[4];
+        O::sample(a.met, ts, xs, ys, zs, 7, w);
+        // stage 0: midpoint from (lon, lat, p) with half a step;
+        // stage 1: full step from (lon, lat, p) with the midpoint winds
+        const double nlon = lon + O::over_cos(w[0] * h * kDegPerM, ys);
+        const double nlat = lat + w[1] * h * kDegPerM;
+        const double np_ = p + w[2] * h;
+        ts = time + half;
+        xs = nlon; ys = nlat; zs = np_;
+        h = dt;
+      }
+      lon = xs; lat = ys; p = zs;
       time = time + dt;
     }
 
@@ -168,7 +186,7 @@ __global__ void __launch_bounds__(256, LT_STEP_MIN_BLOCKS) step_kernel(const Ste
     // post-hop lon/lat and pre-hop p (numpy view aliasing)
     if (want_turb && act) {
       double xt[3];
-      draws<O>(a, s, gid, 1, xt);
+      draws<O, RM>(a, s, gid, 1, xt);
       if (ctl.turb_dx > 0.0) {
         const double sig = sqrt(2.0 * ctl.turb_dx * dt);
         const double nlon = lon + O::over_cos(sig * xt[0] * kDegPerM, lat);
@@ -187,7 +205,7 @@ __global__ void __launch_bounds__(256, LT_STEP_MIN_BLOCKS) step_kernel(const Ste
     // physics.py:150-188 (module_diffusion_meso): AR(1) with met0 cell spread
     if (want_meso && act) {
       double xm[3];
-      draws<O>(a, s, gid, 2, xm);
+      draws<O, RM>(a, s, gid, 2, xm);
       Corners<Rec> q;
       gather(a.met.s0, a.met, O::cell(a.met, lon, lat, p), q);
       double r = 1.0 - 2.0 * dt / ctl.met_dt;
@@ -197,8 +215,8 @@ __global__ void __launch_bounds__(256, LT_STEP_MIN_BLOCKS) step_kernel(const Ste
 #pragma unroll
       for (int f = 0; f < 3; ++f) {
         const double sigma = ctl.turb_meso * O::spread(q, f);
-        pert[f] = r * a.uvwp[f * a.cap + s] + amp * sigma * xm[f];
-        a.uvwp[f * a.cap + s] = pert[f];
+        pert[f] = r * a.uvwp[f][s] + amp * sigma * xm[f];
+        a.uvwp[f][s] = pert[f];
       }
       const double nlon = lon + O::over_cos(pert[0] * dt * kDegPerM, lat);
       lat = lat + pert[1] * dt * kDegPerM;
@@ -209,7 +227,7 @@ __global__ void __launch_bounds__(256, LT_STEP_MIN_BLOCKS) step_kernel(const Ste
     // physics.py:191-203 (module_convection)
     if (want_conv && act) {
       double xc[3];
-      draws<O>(a, s, gid, 0, xc);
+      draws<O, RM>(a, s, gid, 0, xc);
       if (p > ctl.conv_p_top && xc[0] < ctl.conv_prob)
         p = ctl.conv_p_top + (xc[0] / ctl.conv_prob) * (ctl.p_surf - ctl.conv_p_top);
     }

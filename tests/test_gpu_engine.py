@@ -191,3 +191,39 @@ def test_fast_precision_within_north_star_tolerance(eng):
     assert np.abs(fast.lat - exact.lat).max() / 180.0 <= 1e-5
     assert (np.abs(fast.p - exact.p) / exact.p).max() <= 1e-5
     np.testing.assert_array_equal(fast.time, exact.time)
+
+
+@pytest.mark.parametrize("chunk", [0, 700, 2048])
+def test_host_path_equals_device_path_bitwise(eng, golden_chain, chunk):
+    """lt_run_host (host SoA streamed through the store in overlapped
+    chunks, a ring of slots when chunk < n) == the device-resident step."""
+    engine, ms, _ = eng
+    from paper_2211_12616_b200.context import pinned_empty
+    g = golden_chain
+    ctl = chain_ctl()
+    m0, m1 = snapshot_from(g, "m0"), snapshot_from(g, "m1")
+    ref, rc = _run_chain(engine, ms, g, ctl, 6, shards=1)
+    ens = _ens(ms, g, "init")
+    n = ens.np
+    pin = {k: pinned_empty(n) for k in ("time", "p", "lon", "lat")}
+    for k, a in pin.items():
+        a[:] = getattr(ens, k)
+    q = pinned_empty((5, n))
+    q[:] = ens.q
+    host = ms.ParticleEnsemble(n, pin["time"], pin["p"], ens.zeta, pin["lon"], pin["lat"], q)
+    cache = ms.CacheState(uvwp=pinned_empty((3, n)), iso_var=pinned_empty(n))
+    cache.uvwp[:] = 0.0
+    e = engine.Engine(device=0)
+    e.ctx.alloc(1500 if chunk == 700 else n, 5)   # ring of 2 slots for chunk 700
+    e.bind_met(m0, m1)
+    e.load_clim(ms.read_clim(ctl))
+    e.ctx.run_host(ctl, engine.capi.MOD_ISOSURF_INIT, n, 0, 0, host.time, host.p, host.lon,
+                   host.lat, iso_var=cache.iso_var, chunk=chunk)
+    for step in range(6):
+        e.step_host(ctl, host, cache, step, engine.FULL, chunk=chunk)
+    e.close()
+    for k in ("lon", "lat", "p", "time"):
+        np.testing.assert_array_equal(getattr(host, k), getattr(ref, k))
+    np.testing.assert_array_equal(host.q, ref.q)
+    np.testing.assert_array_equal(cache.uvwp, rc.uvwp)
+    np.testing.assert_array_equal(cache.iso_var, rc.iso_var)
