@@ -197,6 +197,21 @@ int lt_field_d2h_ordered(lt_ctx *ctx, int32_t field, int32_t row, int64_t offset
 int lt_field_h2d_ordered(lt_ctx *ctx, int32_t field, int32_t row, int64_t offset,
                          int64_t count, int64_t first_id, const void *host);
 
+/* output-side statistics over particles [start, end) of the store
+   (output.py:28-64), reduced in HBM:
+   lt_grid_counts  write_grid (output.py:28-44): counts[ix * ny + iy] (int64,
+                   nx*ny, overwritten), ix = clip(floor((lon+180)/(360/nx)),0,nx-1)
+   lt_group_stats  write_ens (output.py:47-64): groups = int64(q[slot]) (must
+                   be >= 0), ascending; count and mean/std (ddof 0) of lon,
+                   lat, p.  mean/std are [3][max_groups] (lon, lat, p rows).
+                   *ngroups receives the group count; LT_ERR_RANGE when it
+                   exceeds max_groups (nothing else written), LT_ERR_ARG for a
+                   negative group id (ValueError in the reference). */
+int lt_grid_counts(lt_ctx *ctx, int32_t nx, int32_t ny, int64_t start, int64_t end,
+                   int64_t *counts);
+int lt_group_stats(lt_ctx *ctx, int32_t slot, int64_t start, int64_t end, int64_t max_groups,
+                   int64_t *ngroups, int64_t *gid, int64_t *count, double *mean, double *std);
+
 /* event timing of the last lt_run / lt_sort_by_box on this context */
 int lt_timing(lt_ctx *ctx, int32_t enable);
 int lt_last_elapsed_ms(lt_ctx *ctx, float *ms);

@@ -514,3 +514,29 @@ def full_step(ctl, m0, m1, st, lo, hi, step, rng_state=None, clim=None,
             st["q"][slot, s] = q[slot]
     st["time"][s], st["lon"][s], st["lat"][s], st["p"][s] = time, lon, lat, p
     return new_state
+
+
+# --------------------------------------------------------------------------
+# output-side statistics (output.py:28-64)
+# --------------------------------------------------------------------------
+
+def bin_counts(lon, lat, nx, ny):
+    """Particles per lon/lat bin over [-180,180) x [-90,90], upper edges in
+    the last bin (output.py:33-38: clip(floor((x+off)/w)) then add.at)."""
+    wx, wy = 360.0 / nx, 180.0 / ny
+    ix = np.clip(np.floor((np.asarray(lon) + 180.0) / wx).astype(np.int64), 0, nx - 1)
+    iy = np.clip(np.floor((np.asarray(lat) + 90.0) / wy).astype(np.int64), 0, ny - 1)
+    return np.bincount(ix * ny + iy, minlength=nx * ny).astype(np.int64).reshape(nx, ny)
+
+
+def grouped_moments(qslot, lon, lat, p):
+    """Ascending group ids int64(qslot) (>= 0, else ValueError) with count,
+    mean and population std of lon, lat, p per group (output.py:52-63)."""
+    gids = np.asarray(qslot).astype(np.int64)
+    if np.any(gids < 0):
+        raise ValueError("group ids must be non-negative")
+    groups = np.unique(gids)
+    counts = np.array([np.count_nonzero(gids == g) for g in groups], dtype=np.int64)
+    means = np.array([[np.mean(a[gids == g]) for g in groups] for a in (lon, lat, p)])
+    stds = np.array([[np.std(a[gids == g]) for g in groups] for a in (lon, lat, p)])
+    return groups, counts, means.reshape(3, -1), stds.reshape(3, -1)

@@ -19,7 +19,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIBDIR = PKG / "_lib"
 LIB = LIBDIR / "liblagtrans_b200.so"
-SOURCES = ["lt_capi.cu", "lt_kernels.cu", "lt_step.cu"]
+SOURCES = ["lt_capi.cu", "lt_kernels.cu", "lt_step.cu", "lt_output.cu"]
 HEADERS = ["lt_device.cuh", "lt_step.cuh", "lt_kernels.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "--expt-relaxed-constexpr",

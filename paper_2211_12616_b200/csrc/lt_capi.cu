@@ -966,6 +966,75 @@ int lt_field_h2d_ordered(lt_ctx* c, int32_t field, int32_t row, int64_t off, int
   return ordered_copy(c, field, row, off, cnt, first_id, const_cast<void*>(host), false);
 }
 
+// ------------------------------------------------------------------ output statistics
+
+int lt_grid_counts(lt_ctx* c, int32_t nx, int32_t ny, int64_t start, int64_t end, int64_t* counts) {
+  int rc = check_ctx(c);
+  if (rc || (rc = check_particles(c))) return rc;
+  if (nx < 1 || ny < 1) return fail(LT_ERR_ARG, "grid needs nx, ny >= 1");
+  if (!(0 <= start && start <= end && end <= c->cap))
+    return fail(LT_ERR_RANGE, "range [%lld, %lld) outside ensemble of %lld particles",
+                (long long)start, (long long)end, (long long)c->cap);
+  const size_t nb = static_cast<size_t>(nx) * ny;
+  unsigned long long* dev = nullptr;
+  if ((rc = alloc_dev(reinterpret_cast<void**>(&dev), sizeof(unsigned long long) * nb, "grid counts")))
+    return rc;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  cudaError_t e = cudaMemsetAsync(dev, 0, sizeof(unsigned long long) * nb, c->stream);
+  if (e == cudaSuccess) e = launch_grid_counts(c->lon, c->lat, start, end - start, nx, ny, dev, sms, c->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(counts, dev, sizeof(int64_t) * nb, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  cudaFree(dev);
+  CK(e);
+  return LT_OK;
+}
+
+int lt_group_stats(lt_ctx* c, int32_t slot, int64_t start, int64_t end, int64_t max_groups,
+                   int64_t* ngroups, int64_t* gid, int64_t* count, double* mean, double* std_) {
+  int rc = check_ctx(c);
+  if (rc || (rc = check_particles(c))) return rc;
+  if (slot < 0 || slot >= c->nq)
+    return fail(LT_ERR_ARG, "ens_group_slot %d is not a valid quantity slot", slot);
+  if (!(0 <= start && start <= end && end <= c->cap))
+    return fail(LT_ERR_RANGE, "range [%lld, %lld) outside ensemble of %lld particles",
+                (long long)start, (long long)end, (long long)c->cap);
+  if (max_groups < 0) return fail(LT_ERR_ARG, "max_groups < 0");
+  *ngroups = 0;
+  const int64_t n = end - start;
+  if (n == 0) return LT_OK;
+  const double* qrow = c->q + static_cast<int64_t>(slot) * c->cap;
+  size_t need = 0;
+  int64_t ng = 0;
+  std::vector<uint32_t> g32(std::max<int64_t>(max_groups, 1));
+  std::vector<double> m(3 * std::max<int64_t>(max_groups, 1)), sd(m.size());
+  CK(group_stats(c->lon, c->lat, c->p, qrow, c->ids, start, n, max_groups, nullptr, 0, &need,
+                 c->bad, &ng, g32.data(), count, m.data(), sd.data(), c->stream));
+  void* ws = nullptr;
+  if ((rc = alloc_dev(&ws, need, "group stats workspace"))) return rc;
+  cudaError_t e = cudaMemsetAsync(c->bad, 0, sizeof(int), c->stream);
+  if (e == cudaSuccess)
+    e = group_stats(c->lon, c->lat, c->p, qrow, c->ids, start, n, max_groups, ws, need, &need,
+                    c->bad, &ng, g32.data(), count, m.data(), sd.data(), c->stream);
+  int bad = 0;
+  if (e == cudaSuccess) e = cudaMemcpy(&bad, c->bad, sizeof(int), cudaMemcpyDeviceToHost);
+  cudaFree(ws);
+  CK(e);
+  *ngroups = ng;
+  if (bad) return fail(LT_ERR_ARG, bad == 1 ? "group ids must be non-negative" : "group id exceeds 2^32");
+  if (ng > max_groups)
+    return fail(LT_ERR_RANGE, "%lld groups exceed max_groups %lld", (long long)ng, (long long)max_groups);
+  for (int64_t g = 0; g < ng; ++g) {
+    gid[g] = g32[g];
+    for (int f = 0; f < 3; ++f) {
+      mean[f * max_groups + g] = m[f * ng + g];
+      std_[f * max_groups + g] = sd[f * ng + g];
+    }
+  }
+  return LT_OK;
+}
+
 // ------------------------------------------------------------------ timing / host memory
 
 int lt_timing(lt_ctx* c, int32_t enable) {

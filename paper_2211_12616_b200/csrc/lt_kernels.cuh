@@ -53,6 +53,15 @@ cudaError_t launch_iota(uint32_t* ids, int64_t offset, int64_t count, int64_t fi
                         cudaStream_t st);
 cudaError_t launch_fill(double* x, int64_t n, double v, cudaStream_t st);
 
+cudaError_t launch_grid_counts(const double* lon, const double* lat, int64_t start, int64_t n,
+                               int nx, int ny, unsigned long long* counts, int sms,
+                               cudaStream_t st);
+cudaError_t group_stats(const double* lon, const double* lat, const double* p, const double* qrow,
+                        const uint32_t* ids, int64_t start, int64_t n, int64_t max_groups, void* ws,
+                        size_t ws_bytes, size_t* ws_need, int* bad_dev, int64_t* ngroups_out,
+                        uint32_t* gid_out, int64_t* count_out, double* mean_out, double* std_out,
+                        cudaStream_t st);
+
 template <class Rec>
 cudaError_t launch_step(const StepArgs<Rec>& a, cudaStream_t st);
 

@@ -40,8 +40,12 @@ struct StepArgs {
   Clim clim;
 };
 
+__device__ __forceinline__ void prefetch_l2(const void* ptr) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
+}
+
 #ifndef LT_STEP_MIN_BLOCKS
-#define LT_STEP_MIN_BLOCKS 3
+#define LT_STEP_MIN_BLOCKS 4
 #endif
 
 // Arithmetic policy: EXACT reproduces numpy's operation sequence in fp64;
@@ -127,6 +131,19 @@ __global__ void __launch_bounds__(256, LT_STEP_MIN_BLOCKS) step_kernel(const Ste
 
   for (int64_t s = a.start + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
        s < a.end; s += stride) {
+    // stage the next particle's state rows into L2 while this one runs
+    // (costs no registers; the loads below then hit L2 instead of HBM)
+#ifndef LT_NO_PREFETCH
+    if (s + stride < a.end) {
+      const int64_t nx = s + stride;
+      prefetch_l2(a.time + nx); prefetch_l2(a.lon + nx); prefetch_l2(a.lat + nx);
+      prefetch_l2(a.p + nx);
+      if (mods & M_MESO) {
+        prefetch_l2(a.uvwp[0] + nx); prefetch_l2(a.uvwp[1] + nx); prefetch_l2(a.uvwp[2] + nx);
+      }
+      if (a.ids && (mods & (M_TURB | M_MESO | M_CONVECTION))) prefetch_l2(a.ids + nx);
+    }
+#endif
     double time = a.time[s], lon = a.lon[s], lat = a.lat[s], p = a.p[s];
 
     // physics.py:82-88 (module_timesteps)

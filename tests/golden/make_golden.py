@@ -281,8 +281,30 @@ def gen_sbr():
                         lons=lons, lats=lats, levs=levs, ulat=ulat)
 
 
+def gen_output():
+    """write_grid / write_ens of the reference on a seeded ensemble with
+    bin-edge particles and 5 groups (one a single point)."""
+    import tempfile
+    from lagtrans import output
+    ctl = Control(grid_nx=36, grid_ny=18, ens_group_slot=5, nq=6)
+    ens = particles(ctl, 4000, 33, lat_span=90.0)
+    ens.lon[:6] = [-180.0, 180.0 - 1e-9, 0.0, 10.0, -170.0, 179.99999]
+    ens.lat[:6] = [-90.0, 90.0, 0.0, 10.0, 89.99999, -85.0]
+    rs = np.random.default_rng(34)
+    ens.q[5, :] = rs.integers(0, 4, ens.np) + 0.25
+    ens.q[5, 10:20] = 7.9     # group 7: ten particles at one point
+    ens.lon[10:20], ens.lat[10:20], ens.p[10:20] = 5.0, 6.0, 700.0
+    with tempfile.TemporaryDirectory() as d:
+        output.write_grid(ctl, ens, Path(d) / "grid.csv")
+        output.write_ens(ctl, ens, Path(d) / "ens.csv")
+        grid_csv = (Path(d) / "grid.csv").read_text()
+        ens_csv = (Path(d) / "ens.csv").read_text()
+    np.savez_compressed(OUT / "output.npz", **ens_arrays("ens", ens), grid_nx=36, grid_ny=18,
+                        slot=5, grid_csv=np.array(grid_csv), ens_csv=np.array(ens_csv))
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["interp", "modules", "rng", "chain", "sbr"]
+    which = sys.argv[1:] or ["interp", "modules", "rng", "chain", "sbr", "output"]
     for name in which:
         globals()[f"gen_{name}"]()
         print("wrote", name)

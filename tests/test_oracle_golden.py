@@ -9,7 +9,7 @@ the one that generated the fixtures."""
 import numpy as np
 import pytest
 
-from conftest import chain_ctl, control, modules_ctl, snapshot_from
+from conftest import chain_ctl, control, load_golden, modules_ctl, snapshot_from
 from oracle import lagtrans_oracle as orc
 
 TRANS = dict(rtol=1e-13, atol=1e-300)
@@ -253,3 +253,31 @@ def test_partition_rule():
     assert orc.split_range(3, 4, 3) == (3, 3)
     with pytest.raises(ValueError):
         orc.split_range(10, 2, 2)
+
+
+# ------------------------------------------------------------ output statistics
+
+def _csv_rows(text):
+    return [line.split(",") for line in str(text).splitlines()[1:]]
+
+
+def test_bin_counts_match_reference_write_grid():
+    g = load_golden("output")
+    counts = orc.bin_counts(g["ens_lon"], g["ens_lat"], int(g["grid_nx"]), int(g["grid_ny"]))
+    ref = np.array([int(r[2]) for r in _csv_rows(g["grid_csv"])]).reshape(counts.shape)
+    np.testing.assert_array_equal(counts, ref)
+    assert counts.sum() == g["ens_lon"].size
+
+
+def test_grouped_moments_match_reference_write_ens():
+    g = load_golden("output")
+    gids, cnts, means, stds = orc.grouped_moments(g["ens_q"][int(g["slot"])], g["ens_lon"],
+                                                  g["ens_lat"], g["ens_p"])
+    rows = _csv_rows(g["ens_csv"])
+    assert [int(r[0]) for r in rows] == list(gids)
+    assert [int(r[1]) for r in rows] == list(cnts)
+    ref = np.array([[float(x) for x in r[2:]] for r in rows])   # lon_mean, lon_std, lat_mean ...
+    np.testing.assert_array_equal(ref[:, 0::2].T, means)
+    np.testing.assert_array_equal(ref[:, 1::2].T, stds)
+    with pytest.raises(ValueError):
+        orc.grouped_moments(np.array([1.0, -1.0]), *np.zeros((3, 2)))
