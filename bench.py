@@ -1,22 +1,32 @@
-"""Benchmark: particle-steps/s of the fused advection + diffusion step on B200.
+"""Benchmark: particle-steps/s of the fused time step on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg3|cfg2|cfg1]
-                    [--impl b200|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg3]
+                    [--impl b200|reference] [--precision fast|exact]
 
-Workload (BASELINE.json configs[2], the metric's "at 1/2/4/8 B200" config):
-1e8 particles on the synthetic ERA5-like 0.25 deg grid (1440(+1) x 721 x
-137), advection + turbulent + mesoscale diffusion (+ timesteps, in-kernel
-counter RNG, position), sharded over N GPUs with the reference partition
-rule, met replicated to every rank by an NCCL broadcast.  A "step" is one
-fused time step of every particle; the box sort runs every `--sort-every`
-steps inside the timed region.
+Headline workload (BASELINE.json configs[2], the configuration the metric is
+quoted on): **cfg3** — 1e8 particles on the synthetic ERA5-like 0.25 deg grid
+(1440(+1) x 721 x 137), advection + turbulent + mesoscale diffusion
+(+ timesteps, in-kernel counter RNG, position), sharded over N GPUs with the
+reference partition rule, met replicated to every rank by an NCCL
+broadcast.  A "step" is one fused time step of every particle; the box sort
+runs every `--sort-every` steps inside the timed region.
+
+Other workloads (parity shapes, informational lines): cfg1 (SBR, 1e5,
+advection), cfg2 (1e7, 1 deg), cfg4 (5e7 volcanic point release, advection
++ diffusion + sedimentation + decay, a new met snapshot streamed from pinned
+host memory every simulated hour = every 20 steps, inside the timed region),
+cfg5 (5e8 particles, the full module chain + decay, sort every 10 steps).
 
 `value` is device-timed (CUDA events on the engine stream, max over ranks,
-inputs resident in HBM); `e2e` times the same step through the host-buffer
-C-ABI path (pinned host SoA in, step, SoA out every step).  `cpu_baseline`
-and `--impl reference` time the CPU oracle (a numpy restatement of the
-reference, oracle/) on the host's cores on a bounded particle sample of the
-same workload.
+inputs resident in HBM).  `e2e` is the public host-buffer API
+(Engine.step_host -> lt_run_host): the shard's SoA in pinned host memory
+streams in, steps and streams out every step.  `cpu_baseline` and `--impl
+reference` time the CPU oracle (a numpy restatement of the reference,
+oracle/) on the host's cores on a bounded particle sample of the same
+workload.  `precision` "fast" (default) computes interpolation weights and
+sums and the Box-Muller transform in fp32 with fp64 particle state; it stays
+within the north star's 1e-5 run tolerance (tests/test_gpu_engine.py); the
+line also carries the bit-faithful "exact" kernel's numbers.
 """
 
 from __future__ import annotations
@@ -38,16 +48,37 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "particle-steps/s (advect+diffusion) at 1/2/4/8 B200; % of HBM roofline"
+ADV = ("advection", "position")
+ADV_DIFF = ("advection", "turb", "meso", "position")
+PLUME = ("advection", "turb", "meso", "sedi", "decay", "position")
+FULL = ("advection", "turb", "meso", "convection", "sedi", "decay", "isosurf", "position",
+        "meteo")
 WORKLOADS = {
-    # name: (total particles, dlon, dlat, nlev, p_min, modules, description)
-    "cfg3": (100_000_000, 0.25, 0.25, 137, 0.01, "adv_diff",
-             "1e8 particles, ERA5-like 0.25deg 1440x721x137, advection+turb+meso diffusion"),
-    "cfg2": (10_000_000, 1.0, 1.0, 60, 1.0, "adv_diff",
-             "1e7 particles, ERA5-like 1deg 360x181x60, advection+turb+meso diffusion"),
-    "cfg1": (100_000, 1.0, 1.0, 60, 1.0, "adv",
-             "1e5 particles, solid-body rotation 1deg x 60, advection only"),
+    "cfg1": dict(n=100_000, grid=(1.0, 1.0, 60, 1.0), met="sbr", chain=ADV, init="uniform",
+                 sort_every=0, desc="1e5 particles, solid-body rotation 1deg x 60, advection only"),
+    "cfg2": dict(n=10_000_000, grid=(1.0, 1.0, 60, 1.0), met="era5", chain=ADV_DIFF,
+                 init="uniform", sort_every=10,
+                 desc="1e7 particles, ERA5-like 1deg 360x181x60, advection+turb+meso diffusion"),
+    "cfg3": dict(n=100_000_000, grid=(0.25, 0.25, 137, 0.01), met="era5", chain=ADV_DIFF,
+                 init="uniform", sort_every=10,
+                 desc="1e8 particles, ERA5-like 0.25deg 1440x721x137, advection+turb+meso "
+                      "diffusion"),
+    "cfg4": dict(n=50_000_000, grid=(0.25, 0.25, 137, 0.01), met="stream", chain=PLUME,
+                 init="point", sort_every=0, met_dt=3600.0,
+                 ctl=dict(sedi_radius=5e-6, sedi_density=2000.0, decay_tau=3 * 86400.0,
+                          decay_slot=5, nq=6),
+                 desc="volcanic point release of 5e7 particles (-175.4E, -20.5N, 30 hPa), "
+                      "advection+diffusion+sedimentation+decay, 0.25deg met streamed hourly "
+                      "from pinned host memory"),
+    "cfg5": dict(n=500_000_000, grid=(0.25, 0.25, 137, 0.01), met="era5", chain=FULL,
+                 init="uniform", sort_every=10,
+                 ctl=dict(conv_prob=0.05, sedi_radius=1e-6, isosurf_mode="theta",
+                          decay_tau=3 * 86400.0, decay_slot=5, nq=6),
+                 desc="5e8 particles, full module chain (+decay) with box sort every 10 "
+                      "steps"),
 }
-STATE_BYTES = {"adv": 64, "adv_diff": 112}  # fp64 lon/lat/p/time r+w (+ fp64 uvwp r+w)
+# algorithmic state bytes per particle-step (fp64 rows read + written)
+STATE_BYTES = {ADV: 64, ADV_DIFF: 112, PLUME: 128, FULL: 168}
 
 
 def dist_env():
@@ -57,11 +88,12 @@ def dist_env():
     return ws, rank, local
 
 
-def algorithmic_bytes(mod: str, n_local: int, nodes: int) -> float:
+def algorithmic_bytes(chain, n_local: int, nodes: int) -> float:
     """b = b_state + 32*nodes*(1 - exp(-8 N/nodes)) / N per
-    particle-step (two fp32 float4 snapshots over the touched nodes)."""
+    particle-step (two fp32 snapshots' node-pair records over the touched
+    cells, each read once per step)."""
     b_met = 32.0 * nodes * (1.0 - math.exp(-8.0 * n_local / nodes)) / n_local
-    return STATE_BYTES[mod] + b_met
+    return STATE_BYTES[chain] + b_met
 
 
 class ClockSampler:
@@ -115,27 +147,51 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def build_met(wl, rank, ws, torch, dist):
-    """Rank 0 builds the snapshot pair on the host; with N > 1 ranks it is
-    replicated by an NCCL broadcast (the only data collective of the path)."""
+def make_ctl(wl, precision="fast"):
+    from paper_2211_12616_b200.model_state import Control
+    cfg = WORKLOADS[wl]
+    kw = dict(np_max=10 ** 10, t_stop=30 * 86400.0, dt_model=180.0,
+              met_dt=cfg.get("met_dt", 10800.0), turb_dx=50.0, turb_dz=0.1, turb_meso=0.16,
+              rng_mode="counter", rng_seed_global=12616, precision=precision)
+    kw.update(cfg.get("ctl", {}))
+    return Control(**kw)
+
+
+def make_particles(wl, n, seed):
     from paper_2211_12616_b200 import synthetic
-    n_tot, dlon, dlat, nlev, pmin, mod, _ = WORKLOADS[wl]
-    if wl == "cfg1":
+    cfg = WORKLOADS[wl]
+    nq = cfg.get("ctl", {}).get("nq", 5)
+    if cfg["init"] == "point":
+        ens = synthetic.point_release(n, nq=nq)
+    else:
+        ens = synthetic.particles(n, seed=seed, nq=nq)
+    if nq > 5:
+        ens.q[5] = 1.0   # the decayed tracer mass
+    return ens
+
+
+def build_met(wl, rank, ws):
+    """Rank 0 (or the only rank) builds the first snapshot pair on the host;
+    other ranks only need the grid (the fields arrive by broadcast)."""
+    from paper_2211_12616_b200 import synthetic
+    cfg = WORKLOADS[wl]
+    dlon, dlat, nlev, pmin = cfg["grid"]
+    if cfg["met"] == "sbr":
         return synthetic.solid_body_pair(dlon, dlat, nlev)
+    t1 = cfg.get("met_dt", 10800.0)
     if ws == 1 or rank == 0:
-        return synthetic.analytic_pair(dlon, dlat, nlev, 0.0, 10800.0, pmin)
-    lons, lats, levs = synthetic.grid(dlon, dlat, nlev, pmin)
-    return None, (lons, lats, levs)
+        return synthetic.analytic_pair(dlon, dlat, nlev, 0.0, t1, pmin)
+    return None, synthetic.grid(dlon, dlat, nlev, pmin)
 
 
-def load_met_everywhere(eng, mets, ws, rank, torch, dist):
+def load_met_everywhere(eng, mets, wl, ws, rank, torch, dist):
     """N = 1: H2D of both snapshots.  N > 1: rank 0's snapshots reach every
     rank by NCCL broadcast (sharding.broadcast_snapshot) and are packed into
     the met slots straight from device memory."""
     m0, m1 = mets
     if ws == 1:
         eng.bind_met(m0, m1)
-        return m0, m1
+        return
     from paper_2211_12616_b200 import _capi as capi
     from paper_2211_12616_b200 import sharding
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -146,7 +202,7 @@ def load_met_everywhere(eng, mets, ws, rank, torch, dist):
         grid = (np.append(lons, lons[0] + 360.0), lats, levs)
     eng.set_grid(*grid)
     shape = (len(grid[0]), len(grid[1]), len(grid[2]))
-    for slot, t_met in ((0, 0.0), (1, 10800.0)):
+    for slot, t_met in ((0, 0.0), (1, WORKLOADS[wl].get("met_dt", 10800.0))):
         src = (m0, m1)[slot] if rank == 0 else None
         buf = sharding.broadcast_snapshot(src, shape, dist, dev)
         torch.cuda.synchronize()
@@ -157,7 +213,34 @@ def load_met_everywhere(eng, mets, ws, rank, torch, dist):
         eng.ctx.sync()
         del buf
     eng.ctx.use_met(0, 1)
-    return None, None
+    eng._met_slots, eng._staged = (0, 1), None
+
+
+def streamed_nodes(wl, ws, rank, torch, dist):
+    """cfg4: two hourly snapshots as pinned (nx, ny, nz, 4) fp32 node arrays
+    (without the +360 column); the stream alternates them at increasing
+    t_met.  N > 1: rank 0 builds them and broadcasts."""
+    from paper_2211_12616_b200 import synthetic
+    from paper_2211_12616_b200.context import pinned_empty
+    dlon, dlat, nlev, pmin = WORKLOADS[wl]["grid"]
+    lons, lats, levs = synthetic.grid(dlon, dlat, nlev, pmin)
+    shape = (len(lons), len(lats), len(levs), 4)
+    out = []
+    for phase in (20.0, 30.0):
+        host = pinned_empty(shape, np.float32)
+        if ws == 1 or rank == 0:
+            f = synthetic.era5_like(lons, lats, levs, phase)
+            for c, k in enumerate(("u", "v", "w", "T")):
+                host[..., c] = f[k]
+        if ws > 1:
+            dev = torch.device("cuda", torch.cuda.current_device())
+            buf = torch.from_numpy(host).to(dev) if rank == 0 else \
+                torch.empty(shape, dtype=torch.float32, device=dev)
+            dist.broadcast(buf, src=0)
+            torch.from_numpy(host).copy_(buf.cpu())
+            del buf
+        out.append(host)
+    return out
 
 
 def cpu_sample_rate(wl, mets, ctl, n_sample, steps, threads, target_s=0.0):
@@ -171,34 +254,28 @@ def cpu_sample_rate(wl, mets, ctl, n_sample, steps, threads, target_s=0.0):
     from concurrent.futures import ThreadPoolExecutor
 
     from oracle import lagtrans_oracle as orc
-    from paper_2211_12616_b200 import synthetic
     m0, m1 = mets
-    s0 = orc.Snapshot(m0.t_met, m0.lons, m0.lats, m0.levs, m0.u, m0.v, m0.w, m0.T)
-    s1 = orc.Snapshot(m1.t_met, m1.lons, m1.lats, m1.levs, m1.u, m1.v, m1.w, m1.T)
-    ens = synthetic.particles(n_sample, seed=12616)
+    s0, s1 = orc.Snapshot.like(m0), orc.Snapshot.like(m1)
+    ens = make_particles(wl, n_sample, 12616)
     st = {"time": ens.time.copy(), "lon": ens.lon.copy(), "lat": ens.lat.copy(),
           "p": ens.p.copy(), "uvwp": np.zeros((3, n_sample)), "iso_var": np.zeros(n_sample),
-          "q": np.zeros((5, n_sample))}
-    mods = ("advection", "position") if WORKLOADS[wl][5] == "adv" else \
-        ("advection", "turb", "meso", "position")
+          "q": ens.q.copy()}
+    chain = WORKLOADS[wl]["chain"]
+    clim = orc.climatology_tables() if "meteo" in chain else None
+    if "isosurf" in chain:
+        st["iso_var"] = orc.isosurface_value(ctl, s0, s1, st["lon"], st["lat"], st["p"],
+                                             st["time"], st["iso_var"])
     ranges = [orc.split_range(n_sample, threads, d) for d in range(threads)]
     with ThreadPoolExecutor(threads) as pool:
         def one(step):
-            list(pool.map(lambda r: orc.full_step(ctl, s0, s1, st, r[0], r[1], step, modules=mods),
-                          ranges))
+            list(pool.map(lambda r: orc.full_step(ctl, s0, s1, st, r[0], r[1], step, clim=clim,
+                                                  modules=chain), ranges))
         one(0)  # warm-up
         t0 = time.perf_counter()
         for k in range(steps):
             one(1 + k)
         wall = time.perf_counter() - t0
     return n_sample * steps / wall, wall, n_sample
-
-
-def make_ctl(wl, precision="exact"):
-    from paper_2211_12616_b200.model_state import Control
-    return Control(np_max=10 ** 10, t_stop=10 * 86400.0, dt_model=180.0, met_dt=10800.0,
-                   turb_dx=50.0, turb_dz=0.1, turb_meso=0.16, rng_mode="counter",
-                   rng_seed_global=12616, precision=precision)
 
 
 def host_threads():
@@ -209,13 +286,14 @@ def host_threads():
 
 
 def run_reference(args, wl):
-    """--impl reference: the CPU oracle port of the reference path."""
+    """--impl reference: the CPU oracle port of the reference path on all
+    host threads, rank 0 only."""
     ws, rank, local = dist_env()
     if rank != 0:
         return
-    n_tot, *_, desc = WORKLOADS[wl]
-    mets = build_met(wl, 0, 1, None, None)
-    ctl = make_ctl(wl)
+    cfg = WORKLOADS[wl]
+    mets = build_met(wl, 0, 1)
+    ctl = make_ctl(wl, "exact")
     threads = host_threads()
     n_sample = args.cpu_sample or (100_000 if wl == "cfg1" else 20_000 * threads)
     rates = []
@@ -223,16 +301,16 @@ def run_reference(args, wl):
         r, wall, n_used = cpu_sample_rate(wl, mets, ctl, n_sample, 2, threads, target_s=10.0)
         rates.append(r)
     v = statistics.median(rates)
-    n_sample = n_used
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "particle-steps/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * n_tot / v, "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": 1e3 * cfg["n"] / v, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": wl, "description": desc, "particles": n_tot},
+        "config": {"workload": wl, "description": cfg["desc"], "particles": cfg["n"]},
         "cpu_baseline": {"value": v, "unit": "particle-steps/s", "cores": threads,
                          "kind": "port",
-                         "sample": f"{n_sample} particles x 2 steps per repeat on the same met grid"},
+                         "sample": f"{n_used} particles x 2 steps per repeat on the same met "
+                                   f"grid, {len(rates)} repeats (median)"},
         "e2e": {"value": v, "unit": "particle-steps/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }), flush=True)
@@ -245,11 +323,13 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="cfg3", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
-    ap.add_argument("--sort-every", type=int, default=10)
+    ap.add_argument("--sort-every", type=int, default=-1)
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--alt-steps", type=int, default=-1,
+                    help="timed steps with the other precision's kernels (default: --steps)")
     ap.add_argument("--cpu-sample", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--precision", default="exact", choices=("exact", "fast"))
+    ap.add_argument("--precision", default="fast", choices=("exact", "fast"))
     ap.add_argument("--met-store", default="f32", choices=("f32", "f64"))
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -261,30 +341,48 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_2211_12616_b200 import engine, sharding, synthetic
+    from paper_2211_12616_b200 import engine, sharding
 
+    cfg = WORKLOADS[wl]
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
     if ws > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    n_tot, dlon, dlat, nlev, pmin, mod, desc = WORKLOADS[wl]
-    mask = engine.ADV if mod == "adv" else engine.ADV_DIFF
+    n_tot = cfg["n"]
+    mask = engine.modules_mask(cfg["chain"])
     work = sharding.shard_range(n_tot, ws, rank)
     ctl = make_ctl(wl, args.precision)
 
-    mets = build_met(wl, rank, ws, torch, dist)
-    eng = engine.Engine(device=local, first_id=work.start, met_precision=args.met_store)
-    ens = synthetic.particles(work.size, seed=12616 + rank)
+    mets = build_met(wl, rank, ws)
+    eng = engine.Engine(device=local, first_id=work.start, met_precision=args.met_store,
+                        nq=ctl.nq)
+    ens = make_particles(wl, work.size, 12616 + rank)
     eng.upload(ens)
-    m0, m1 = load_met_everywhere(eng, mets, ws, rank, torch, dist)
-    nodes = (eng.ctx._grid_key and 1) and None
-    nx = len(mets[0].lons) if mets[0] is not None else len(mets[1][0]) + 1
-    lats_n = len(mets[0].lats) if mets[0] is not None else len(mets[1][1])
-    nlev_n = len(mets[0].levs) if mets[0] is not None else len(mets[1][2])
-    nodes = nx * lats_n * nlev_n
+    load_met_everywhere(eng, mets, wl, ws, rank, torch, dist)
+    if "meteo" in cfg["chain"]:
+        from paper_2211_12616_b200.model_state import read_clim
+        eng.load_clim(read_clim(ctl))
+    eng.init_isosurf(ctl)
+    dlon, dlat, nlev, pmin = cfg["grid"]
+    nodes = (int(round(360.0 / dlon)) + 1) * (int(round(180.0 / dlat)) + 1) * nlev
 
-    stream = torch.cuda.ExternalStream(eng.ctx.stream_handle())
-    sort_every = args.sort_every if mod != "adv" or work.size > 10 ** 6 else 0
+    # met streaming (cfg4): the next snapshot is staged on the copy stream
+    # right after every rotation; rotation follows driver_cli.py:139-149
+    stream = None
+    if cfg["met"] == "stream":
+        stream = {"nodes": streamed_nodes(wl, ws, rank, torch, dist), "k": 0,
+                  "t1": cfg["met_dt"], "rotations": 0}
+
+        def stage_next():
+            s = stream
+            eng.prefetch(nodes=s["nodes"][s["k"] % 2].ctypes.data,
+                         t_met=s["t1"] + cfg["met_dt"], close_lon=True)
+            s["k"] += 1
+        stage_next()
+    t_model = [0.0]
+
+    stream_h = torch.cuda.ExternalStream(eng.ctx.stream_handle())
+    sort_every = args.sort_every if args.sort_every >= 0 else cfg["sort_every"]
 
     def barrier():
         eng.sync()
@@ -294,47 +392,88 @@ def main():
 
     step = 0
     n_sorts = 0
-    for _ in range(args.warmup):
+
+    def one_step(c, record=None):
+        nonlocal step, n_sorts
+        t_next = t_model[0] + ctl.dt_model
+        if stream is not None and stream["t1"] < t_next:   # rotate + stage the next hour
+            eng.rotate()
+            stream["t1"] += cfg["met_dt"]
+            stream["rotations"] += 1
+            stage_next()
         if sort_every and step % sort_every == 0:
             eng.sort()
-        eng.step(ctl, step, mask)
+            n_sorts += 1
+        if record:
+            record[0].record(stream_h)
+        eng.step(c, step, mask)
+        if record:
+            record[1].record(stream_h)
         step += 1
+        t_model[0] = t_next
+
+    for _ in range(args.warmup):
+        one_step(ctl)
     barrier()
 
-    # timed region: K steps, CUDA events on the engine stream around each launch
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps + 2)]
-    with ClockSampler(local) as clk:
-        ev[0].record(stream)
-        for k in range(args.steps):
-            if sort_every and step % sort_every == 0:
-                eng.sort()
-                n_sorts += 1
-            ev[2 + 2 * k].record(stream)
-            eng.step(ctl, step, mask)
-            ev[3 + 2 * k].record(stream)
-            step += 1
-        ev[1].record(stream)
-        barrier()
-    total_ms = ev[0].elapsed_time(ev[1])
-    kern_ms = [ev[2 + 2 * k].elapsed_time(ev[3 + 2 * k]) for k in range(args.steps)]
-    total_ms, kern_avg = sharding.max_over_ranks([total_ms, statistics.mean(kern_ms)], dist,
-                                                 "cuda")
+    def timed(c, k_steps):
+        sorts0 = n_sorts
+        rot0 = stream["rotations"] if stream else 0
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * k_steps + 2)]
+        with ClockSampler(local) as clk:
+            ev[0].record(stream_h)
+            for k in range(k_steps):
+                one_step(c, (ev[2 + 2 * k], ev[3 + 2 * k]))
+            ev[1].record(stream_h)
+            barrier()
+        total = ev[0].elapsed_time(ev[1])
+        kern = statistics.mean(ev[2 + 2 * k].elapsed_time(ev[3 + 2 * k]) for k in range(k_steps))
+        total, kern = sharding.max_over_ranks([total, kern], dist, "cuda")
+        return total, kern, clk.summary(), n_sorts - sorts0, \
+            (stream["rotations"] - rot0 if stream else 0)
+
+    total_ms, kern_avg, clocks, sorts_timed, rots = timed(ctl, args.steps)
     value = n_tot * args.steps / (total_ms / 1e3)
+    b = algorithmic_bytes(cfg["chain"], work.size, nodes)
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
+        if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    peak = peaks.get("hbm_gbs", 6650.0)
+    achieved = b * work.size / (kern_avg / 1e3) / 1e9
+
+    # the other precision's kernels on the same state, same protocol
+    other = None
+    k_other = args.steps if args.alt_steps < 0 else args.alt_steps
+    if k_other > 0:
+        alt = "exact" if args.precision == "fast" else "fast"
+        t2, k2, clk2, _, _ = timed(make_ctl(wl, alt), k_other)
+        other = {"precision": alt, "value": n_tot * k_other / (t2 / 1e3),
+                 "ms_per_step": t2 / k_other, "kernel_ms": k2,
+                 "roofline_frac": b * work.size / (k2 / 1e3) / 1e9 / peak, "steps": k_other,
+                 "clocks": clk2}
 
     # e2e: the public host-buffer API (Engine.step_host -> lt_run_host): the
     # shard's SoA sits in pinned host memory; every step streams it through
     # the GPU (H2D, fused step, D2H overlapped in chunks) and lands back.
     e2e = None
-    if args.e2e_steps > 0:
+    if args.e2e_steps > 0 and stream is None:
+        from paper_2211_12616_b200 import _capi as capi
         from paper_2211_12616_b200 import model_state as ms
         from paper_2211_12616_b200.context import pinned_empty
         n = work.size
+        want_q = any(m in cfg["chain"] for m in ("meteo", "decay"))
+        want_iso = "isosurf" in cfg["chain"]
         hens = ms.ParticleEnsemble(n, pinned_empty(n), pinned_empty(n), np.zeros(1),
-                                   pinned_empty(n), pinned_empty(n), np.zeros((5, 1)))
-        hcache = ms.CacheState(uvwp=pinned_empty((3, n)), iso_var=np.zeros(1))
+                                   pinned_empty(n), pinned_empty(n),
+                                   pinned_empty((ctl.nq, n)) if want_q else np.zeros((5, 1)))
+        hcache = ms.CacheState(uvwp=pinned_empty((3, n)),
+                               iso_var=pinned_empty(n) if want_iso else np.zeros(1))
         for k in ("time", "p", "lon", "lat"):
             getattr(hens, k)[:] = getattr(ens, k)
+        if want_q:
+            hens.q[:] = ens.q
         hcache.uvwp[:] = 0.0
+        if want_iso:
+            eng.ctx.d2h_ordered(capi.F_ISO_VAR, 0, 0, n, eng.first_id, out=hcache.iso_var)
         eng.step_host(ctl, hens, hcache, step, mask)   # warm-up (allocations, events)
         step += 1
         barrier()
@@ -344,56 +483,63 @@ def main():
             step += 1
         barrier()
         te = sharding.max_over_ranks([time.perf_counter() - t0], dist, "cuda")[0]
-        rows_in = 4 + (3 if mod != "adv" else 0)
-        rows_out = rows_in
+        chain = cfg["chain"]
+        rows_in = 4 + (3 if "meso" in chain else 0) + (1 if want_iso else 0) + \
+            (1 if "decay" in chain else 0)
+        rows_out = 4 + (3 if "meso" in chain else 0) + \
+            (5 if "meteo" in chain else (1 if "decay" in chain else 0))
         e2e = {"value": n_tot * args.e2e_steps / te, "unit": "particle-steps/s",
                "h2d_bytes_per_step": 8 * rows_in * n_tot, "d2h_bytes_per_step": 8 * rows_out * n_tot,
+               "steps": args.e2e_steps,
                "path": "Engine.step_host -> lt_run_host: pinned host SoA, chunked H2D / fused "
-                       "step / D2H on three streams, every step"}
+                       "step / D2H on three streams, every step (wall clock, max over ranks)"}
 
-    # roofline of the dominant kernel (step_kernel), algorithmic bytes
-    b = algorithmic_bytes(mod, work.size, nodes)
-    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
-        if (ROOT / "MEASURED_PEAKS.json").exists() else {}
-    peak = peaks.get("hbm_gbs", 6650.0)
-    achieved = b * work.size / (kern_avg / 1e3) / 1e9
     traffic = None
     prof = ROOT / "profiles" / f"ncu_step_{wl}.json"
     if prof.exists():
-        traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+        pj = json.loads(prof.read_text()).get(args.precision, {})
+        if pj.get("dram_bytes_per_particle_step") is not None:
+            traffic = pj["dram_bytes_per_particle_step"] * work.size
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         threads = host_threads()
         n_sample = args.cpu_sample or (100_000 if wl == "cfg1" else 20_000 * threads)
-        mh = mets if wl == "cfg1" else (m0, m1)
-        rate, wall, n_sample = cpu_sample_rate(wl, mh, make_ctl(wl), n_sample, 2, threads,
-                                               target_s=15.0)
+        rate, wall, n_sample = cpu_sample_rate(wl, mets, make_ctl(wl, "exact"), n_sample, 2,
+                                               threads, target_s=15.0)
         cpu = {"value": rate, "unit": "particle-steps/s", "cores": threads, "kind": "port",
                "sample": f"oracle/ numpy port, {n_sample} particles x 2 timed steps on the "
                          f"same {wl} met grid ({wall:.1f} s)"}
 
-    launches = args.steps + n_sorts * 13  # keys 1 + CUB 6 + row gathers 5 + ids 1
+    # launches of our kernels in the headline timed region: one fused step
+    # per step; per sort: keys 1 + CUB radix sort 6 + row gathers 5 + ids 1;
+    # per streamed snapshot: one packing kernel
+    launches = args.steps + sorts_timed * 13 + rots
     if rank == 0:
         print(json.dumps({
             "metric": METRIC, "value": value, "unit": "particle-steps/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic",
-            "config": {"workload": wl, "description": desc, "particles": n_tot,
+            "dtype": "f64 state / f32 interpolation" if args.precision == "fast" else "f64",
+            "data": "synthetic",
+            "config": {"workload": wl, "description": cfg["desc"], "particles": n_tot,
                        "particles_per_gpu": work.size, "met_nodes": nodes,
+                       "modules": list(cfg["chain"]),
                        "met_store": f"{args.met_store} node-pair records", "state": "fp64 SoA",
                        "precision": args.precision,
-                       "rng": "counter (bit-identical to reference), in-kernel",
-                       "sort_every": sort_every, "parallelism": f"particles sharded x{ws}",
-                       "l2": "inputs larger than L2 (state %.1f GB/GPU)" % (
-                           work.size * 144 / 1e9)},
+                       "rng": "counter (reference splitmix64 words), in-kernel",
+                       "sort_every": sort_every, "met_rotations_timed": rots,
+                       "parallelism": f"particles sharded x{ws}, met replicated (NCCL broadcast)",
+                       "l2": "inputs larger than L2 (state %.1f GB/GPU, met %.1f GB)" % (
+                           work.size * 120 / 1e9, 2 * nodes * 16 / 1e9)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "step_kernel", "kernel_ms": kern_avg,
                          "algorithmic_bytes_per_particle_step": b,
-                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
-            "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks
+                         else "fallback"},
+            "alt_precision": other,
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": launches,
         }), flush=True)
     eng.close()

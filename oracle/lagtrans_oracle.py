@@ -477,6 +477,7 @@ def split_range(n, parts, part):
 def full_step(ctl, m0, m1, st, lo, hi, step, rng_state=None, clim=None,
               modules=("advection", "turb", "meso", "convection", "sedi",
                        "isosurf", "position", "meteo")):
+    # decay (new module, not in the reference) runs after sedi when listed
     """Advance particles [lo, hi) of the state dict `st` by one step.
 
     st holds arrays time, lon, lat, p, uvwp(3,n), iso_var, q(nq,n).
@@ -504,6 +505,9 @@ def full_step(ctl, m0, m1, st, lo, hi, step, rng_state=None, clim=None,
         p = convective_mix(ctl, dt, conv, p)
     if "sedi" in modules:
         p = settle(ctl, m0, m1, dt, lon, lat, p, time)
+    slot = getattr(ctl, "decay_slot", -1)
+    if "decay" in modules and 0 <= slot < st["q"].shape[0]:
+        st["q"][slot, s] = decay_factor(ctl, dt, st["q"][slot, s])
     if "isosurf" in modules:
         p, _ = isosurface_pull(ctl, m0, m1, lon, lat, p, time, st["iso_var"][s])
     if "position" in modules:

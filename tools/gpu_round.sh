@@ -1,18 +1,22 @@
 #!/bin/bash
-# One gpurun pass: GPU tests, smoke, bench lines, ncu launch list + full capture
-# of the step kernel.  Everything lands in gpurun_out/.
-set -x
+# One gpurun pass: GPU tests, smoke, bench lines, fast-vs-exact error
+# distribution, ncu launch list + full captures of the step kernel (both
+# precisions).  Everything lands in gpurun_out/.
 OUT=gpurun_out
 mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > $OUT/gpu.txt 2>&1
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > $OUT/smoke.log 2>&1
 timeout 900 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.log 2>&1
 timeout 900 python bench.py ${BENCH_ARGS} > $OUT/bench.log 2>&1
+timeout 600 python tools/fast_error.py > $OUT/fast_error.log 2>&1
 if [ -n "$EXTRA_BENCH" ]; then timeout 900 python bench.py $EXTRA_BENCH > $OUT/bench_extra.log 2>&1; fi
 if [ -z "$NO_NCU" ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
-    --log-file $OUT/launches.csv python bench.py --steps 12 --warmup 3 --no-cpu --e2e-steps 0 ${NCU_ARGS} > $OUT/ncu_launch_run.log 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:step_kernel -s 3 -c 1 \
-    -f -o $OUT/step_full python bench.py --steps 2 --warmup 3 --no-cpu --e2e-steps 0 ${NCU_ARGS} > $OUT/ncu_full_run.log 2>&1
+    --log-file $OUT/launches.csv python bench.py --steps 12 --warmup 3 --no-cpu --e2e-steps 0 --alt-steps 0 > $OUT/ncu_launch_run.log 2>&1
+  for prec in fast exact; do
+    timeout 900 ncu --set full --clock-control none --import-source on -k regex:step_kernel -s 3 -c 1 \
+      -f -o $OUT/step_${prec} python bench.py --steps 2 --warmup 3 --no-cpu --e2e-steps 0 --alt-steps 0 \
+      --precision $prec > $OUT/ncu_${prec}.log 2>&1
+  done
 fi
 ls -la $OUT
