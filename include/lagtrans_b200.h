@@ -147,6 +147,11 @@ int lt_met_load(lt_ctx *ctx, int32_t slot, double t_met, int32_t src_bytes,
 int lt_met_load_nodes(lt_ctx *ctx, int32_t slot, double t_met, const float *uvwT,
                       uint32_t flags);
 int lt_met_use(lt_ctx *ctx, int32_t slot0, int32_t slot1);
+/* replicate a packed snapshot to another context (peer copy over NVLink;
+   a device-to-device copy when both share a GPU) — the single-process
+   met broadcast replacing the per-device deep copies of
+   device_runtime.py:178-186; both contexts must hold the same grid */
+int lt_met_copy_slot(lt_ctx *dst, int32_t dst_slot, lt_ctx *src, int32_t src_slot);
 int lt_met_slot_time(lt_ctx *ctx, int32_t slot, double *t_met);
 
 /* climatology tables for module_meteo (ClimData model_state.py:156-181) */

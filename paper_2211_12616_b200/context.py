@@ -175,16 +175,23 @@ class DeviceContext:
                                               capi.MET_CLOSE_LON if close_lon else 0))
         self._slot_keys[slot] = key
 
+    def copy_slot_from(self, src: "DeviceContext", src_slot: int, slot: int, key=None) -> None:
+        """Replicate src's packed snapshot into `slot` (peer copy / D2D)."""
+        capi.check(self.lib.lt_met_copy_slot(self.h, slot, src.h, src_slot))
+        self._slot_keys[slot] = key if key is not None else src._slot_keys[src_slot]
+
     def use_met(self, slot0: int, slot1: int) -> None:
         capi.check(self.lib.lt_met_use(self.h, slot0, slot1))
 
     def slot_key(self, slot: int):
         return self._slot_keys[slot]
 
-    def bind_pair(self, met0, met1) -> tuple[int, int]:
+    def bind_pair(self, met0, met1, donor=None) -> tuple[int, int]:
         """Make (met0, met1) the active snapshot pair, uploading only what
-        changed (module-API path; grids must be identical).  Returns the
-        (met0, met1) slot numbers."""
+        changed (module-API path; grids must be identical).  `donor(key)`
+        may name another context already holding a snapshot — (ctx, slot) —
+        which is then replicated GPU to GPU instead of uploaded again.
+        Returns the (met0, met1) slot numbers."""
         for name in ("lons", "lats", "levs"):
             if not np.array_equal(np.asarray(getattr(met0, name)), np.asarray(getattr(met1, name))):
                 raise ValueError("met0 and met1 must share one grid on the B200 met store")
@@ -203,10 +210,21 @@ class DeviceContext:
             if key in slots:
                 continue
             free = next(s for s in range(3) if s not in slots.values())
-            self.load_met(free, met, key)
+            src = donor(key) if donor is not None else None
+            if src is not None and src[0] is not self and src[0]._grid_key == self._grid_key:
+                self.copy_slot_from(src[0], src[1], free, key)
+            else:
+                self.load_met(free, met, key)
             slots[key] = free
         self.use_met(slots[k0], slots[k1])
         return slots[k0], slots[k1]
+
+    def find_slot(self, key):
+        """Slot holding the snapshot with fingerprint `key`, or None."""
+        for s in range(3):
+            if self._slot_keys[s] == key:
+                return s
+        return None
 
     def load_clim(self, clim) -> None:
         lat, pg = _f64(clim.lat_grid), _f64(clim.p_grid)

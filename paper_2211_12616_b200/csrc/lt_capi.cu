@@ -603,6 +603,33 @@ int lt_met_use(lt_ctx* c, int32_t s0, int32_t s1) {
   return LT_OK;
 }
 
+// Replicate a packed snapshot GPU to GPU (NVLink peer copy, or a D2D copy
+// when both contexts share a GPU): the single-process counterpart of the
+// met broadcast.  The copy runs on the destination's copy stream after the
+// source slot's packing; the destination slot's ready event follows it.
+int lt_met_copy_slot(lt_ctx* dst, int32_t dslot, lt_ctx* src, int32_t sslot) {
+  int rc = check_ctx(src);
+  if (rc || (rc = check_ctx(dst))) return rc;
+  if (sslot < 0 || sslot > 2) return fail(LT_ERR_ARG, "met slot %d outside [0, 3)", sslot);
+  if (!src->slots[sslot].valid) return fail(LT_ERR_STATE, "source met slot %d not loaded", sslot);
+  if (dst->nx != src->nx || dst->ny != src->ny || dst->nz != src->nz || dst->prec != src->prec)
+    return fail(LT_ERR_ARG, "met grids of the two contexts differ (call lt_met_grid first)");
+  if ((rc = met_prepare(dst, dslot))) return rc;  // also orders after dst's compute
+  const size_t bytes = rec_bytes(src) * n_rec(src);
+  CK(cudaStreamWaitEvent(dst->copy, src->slots[sslot].ready, 0));
+  if (dst->device == src->device)
+    CK(cudaMemcpyAsync(dst->slots[dslot].rec, src->slots[sslot].rec, bytes, cudaMemcpyDeviceToDevice, dst->copy));
+  else
+    CK(cudaMemcpyPeerAsync(dst->slots[dslot].rec, dst->device, src->slots[sslot].rec, src->device, bytes, dst->copy));
+  CK(cudaEventRecord(dst->slots[dslot].ready, dst->copy));
+  // the source slot must not be refilled (on src's copy stream) before this
+  // copy has read it
+  CK(cudaStreamWaitEvent(src->copy, dst->slots[dslot].ready, 0));
+  dst->slots[dslot].t_met = src->slots[sslot].t_met;
+  dst->slots[dslot].valid = true;
+  return LT_OK;
+}
+
 int lt_met_slot_time(lt_ctx* c, int32_t slot, double* t) {
   int rc = check_ctx(c);
   if (rc) return rc;

@@ -44,6 +44,10 @@ __device__ __forceinline__ void prefetch_l2(const void* ptr) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
 }
 
+__device__ __forceinline__ void prefetch_l1(const void* ptr) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(ptr));
+}
+
 #ifndef LT_STEP_MIN_BLOCKS
 #define LT_STEP_MIN_BLOCKS 4
 #endif
@@ -144,6 +148,11 @@ __global__ void __launch_bounds__(256, LT_STEP_MIN_BLOCKS) step_kernel(const Ste
       if (a.ids && (mods & (M_TURB | M_MESO | M_CONVECTION))) prefetch_l2(a.ids + nx);
     }
 #endif
+#ifdef LT_PF_L1_UVWP
+    if (mods & M_MESO) {
+      prefetch_l1(a.uvwp[0] + s); prefetch_l1(a.uvwp[1] + s); prefetch_l1(a.uvwp[2] + s);
+    }
+#endif
     double time = a.time[s], lon = a.lon[s], lat = a.lat[s], p = a.p[s];
 
     // physics.py:82-88 (module_timesteps)
@@ -221,6 +230,13 @@ __global__ void __launch_bounds__(256, LT_STEP_MIN_BLOCKS) step_kernel(const Ste
 
     // physics.py:150-188 (module_diffusion_meso): AR(1) with met0 cell spread
     if (want_meso && act) {
+#ifdef LT_MESO_EARLY
+      // issue the AR(1) state loads before the draws and the gather so
+      // their latency overlaps that work
+      double up[3];
+#pragma unroll
+      for (int f = 0; f < 3; ++f) up[f] = a.uvwp[f][s];
+#endif
       double xm[3];
       draws<O, RM>(a, s, gid, 2, xm);
       Corners<Rec> q;
@@ -232,7 +248,11 @@ __global__ void __launch_bounds__(256, LT_STEP_MIN_BLOCKS) step_kernel(const Ste
 #pragma unroll
       for (int f = 0; f < 3; ++f) {
         const double sigma = ctl.turb_meso * O::spread(q, f);
+#ifdef LT_MESO_EARLY
+        pert[f] = r * up[f] + amp * sigma * xm[f];
+#else
         pert[f] = r * a.uvwp[f][s] + amp * sigma * xm[f];
+#endif
         a.uvwp[f][s] = pert[f];
       }
       const double nlon = lon + O::over_cos(pert[0] * dt * kDegPerM, lat);

@@ -137,7 +137,8 @@ class DeviceImage:
     """One device's data region: an Engine (lt_ctx) holding the owned range
     [base, base + n) of the global ensemble."""
 
-    def __init__(self, gpu: int, host: ModelImage, work: WorkRange, with_batch: bool = True):
+    def __init__(self, gpu: int, host: ModelImage, work: WorkRange, with_batch: bool = True,
+                 donor=None):
         n_total = int(host.ens.np)
         nq = int(host.ens.q.shape[0])
         self.gpu = gpu
@@ -155,6 +156,7 @@ class DeviceImage:
         self.clim = host.clim
         self.met0 = None
         self.met1 = None
+        self.donor = donor   # key -> (context, slot) of another device holding it
 
     # -- module execution (physics._run dispatches here) -------------------
     def local(self, work: WorkRange) -> tuple[int, int]:
@@ -166,7 +168,7 @@ class DeviceImage:
 
     def bind(self, met0, met1) -> None:
         if met0 is not self.met0 or met1 is not self.met1:
-            self.engine.bind_pair(met0, met1)
+            self.engine.bind_pair(met0, met1, self.donor)
             self.met0, self.met1 = met0, met1
 
     def run_module(self, module: int, ctl, work: WorkRange, met0=None, met1=None, clim=None,
@@ -369,7 +371,7 @@ class DevicePool:
         work = work_range or WorkRange(device_id, 0, int(host.ens.np))
         gpu = self.device_map[device_id]
         image = self._executors[device_id].submit(
-            lambda: DeviceImage(gpu, host, work, with_batch)).result()
+            lambda: DeviceImage(gpu, host, work, with_batch, donor=self._met_donor)).result()
         region = DeviceRegion(device_id=device_id, state="created", image=image,
                               work_range=work_range)
         self._regions[device_id] = region
@@ -417,6 +419,19 @@ class DevicePool:
         self._executors[region.device_id].submit(img.close).result()
         region.image = None
         region.state = "deleted"
+
+    def _met_donor(self, key):
+        """A live image already holding snapshot `key`: new images replicate
+        it GPU to GPU (peer copy over NVLink) instead of re-uploading it
+        from the host — the met broadcast of the paper's design."""
+        for region in self._regions.values():
+            img = region.image
+            if img is None:
+                continue
+            slot = img.engine.ctx.find_slot(key)
+            if slot is not None:
+                return img.engine.ctx, slot
+        return None
 
     def region(self, device_id: int) -> DeviceRegion:
         return self._regions[device_id]

@@ -120,12 +120,23 @@ def run_simulation(ctl, ens, mets, num_devices: int = 1, *, fused: bool = True,
             physics.module_isosurf_init(img.ctl, img.ens, met0, met1, img.cache, ranges[d])
         pool.for_each_device_parallel(init, parallel=parallel)
 
-        # fused mode: the next snapshot is staged into each device's free slot
+        # fused mode: device 0 stages the next snapshot from the host into its
+        # free slot; the other devices replicate it GPU to GPU
         def prefetch(d):
             if rest:
-                regions[d].image.engine.prefetch(met=rest[0])
+                eng0 = regions[0].image.engine
+                if d == 0:
+                    eng0.prefetch(met=rest[0])
+                else:
+                    regions[d].image.engine.prefetch_from(eng0)
+
+        def prefetch_all():
+            pool.dispatch(0, lambda: prefetch(0)).result()
+            if num_devices > 1:
+                for d in range(1, num_devices):
+                    pool.dispatch(d, lambda d=d: prefetch(d)).result()
         if fused:
-            pool.for_each_device_parallel(prefetch, parallel=parallel)
+            prefetch_all()
 
         t = ctl.t_start
         next_out = ctl.t_start + ctl.output_dt
@@ -150,7 +161,7 @@ def run_simulation(ctl, ens, mets, num_devices: int = 1, *, fused: bool = True,
                               lambda d=d: pool.region_update_device(regions[d], host,
                                                                     ("met0", "met1")))
                 if fused:
-                    pool.for_each_device_parallel(prefetch, parallel=parallel)
+                    prefetch_all()
 
             if fused:
                 def device_step(d, step=step):

@@ -120,9 +120,10 @@ class Engine:
         self._staged = None
         self.ctx.use_met(0, 1)
 
-    def bind_pair(self, met0, met1) -> None:
-        """Select (met0, met1), uploading only snapshots the slots lack."""
-        self._met_slots = self.ctx.bind_pair(met0, met1)
+    def bind_pair(self, met0, met1, donor=None) -> None:
+        """Select (met0, met1), uploading only snapshots the slots lack
+        (or replicating them from a donor context, see DeviceContext)."""
+        self._met_slots = self.ctx.bind_pair(met0, met1, donor)
         self._staged = None
 
     def set_grid(self, lons, lats, levs) -> None:
@@ -139,6 +140,15 @@ class Engine:
         compute stream keeps stepping on the current pair meanwhile."""
         free = min({0, 1, 2} - set(self._met_slots))
         self.load_slot(free, met=met, nodes=nodes, t_met=t_met, close_lon=close_lon)
+        self._staged = free
+
+    def prefetch_from(self, other: "Engine") -> None:
+        """Stage the snapshot `other` has staged by a GPU-to-GPU copy
+        (NVLink peer copy) instead of another host upload."""
+        if other._staged is None:
+            raise RuntimeError("prefetch_from() an engine without a staged snapshot")
+        free = min({0, 1, 2} - set(self._met_slots))
+        self.ctx.copy_slot_from(other.ctx, other._staged, free)
         self._staged = free
 
     def rotate(self) -> None:

@@ -310,3 +310,32 @@ def test_chain_50_steps_module_api(b200, golden_chain):
     for k in ("lon", "lat", "p"):
         np.testing.assert_allclose(getattr(ens, k), g[f"final_{k}"], rtol=1e-9, atol=1e-9)
     np.testing.assert_allclose(ens.q, g["final_q"], rtol=1e-9, atol=1e-9)
+
+
+def test_interpolate_irregular_axes_bit_exact(b200):
+    """Irregular lon/lat axes (random, jittered; not fp32-representable lat
+    nodes) with particles on the nodes: cell indices and values bit-exact."""
+    phys, _, ms = b200
+    rs = np.random.default_rng(17)
+    lons = np.sort(rs.uniform(-180, 180, 40)).astype(np.float32).astype(np.float64)
+    lats = np.linspace(-90, 90, 31)
+    lats[1:-1] += rs.uniform(-1.5, 1.5, 29)
+    levs = np.geomspace(1000.0, 5.0, 12).astype(np.float32).astype(np.float64)
+    shape = (lons.size, lats.size, levs.size)
+    f = lambda: rs.uniform(-20, 20, shape).astype(np.float32).astype(np.float64)
+    m0 = ms.MeteoField(0.0, lons, lats, levs, f(), f(), f(), rs.uniform(200, 300, shape).astype(
+        np.float32).astype(np.float64))
+    m1 = ms.MeteoField(3600.0, lons, lats, levs, f(), f(), f(),
+                       (m0.T + 1.0).astype(np.float32).astype(np.float64))
+    n = 20000
+    lon = rs.uniform(-200, 200, n)
+    lat = rs.uniform(-95, 95, n)
+    p = rs.uniform(1, 1100, n)
+    lon[:40] = lons          # on nodes: searchsorted-left edge cases
+    lat[:31] = lats
+    p[:12] = levs
+    t = rs.uniform(-100, 4000, n)
+    got = np.stack(phys.interpolate_met(m0, m1, t, lon, lat, p))
+    ref = np.stack(orc.sample(orc.Snapshot.like(m0), orc.Snapshot.like(m1), t, lon, lat, p,
+                              ("u", "v", "w", "T")))
+    exact(got, ref)

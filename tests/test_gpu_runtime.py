@@ -160,3 +160,38 @@ def test_module_mode_timer_contract(rt, golden_chain):
         assert ("INIT", "ACC_INIT", f"device{d}") in keys
         assert ("MEMORY", "DELETE_DATA_REGION", f"device{d}") in keys
     assert all(ns >= 0 for *_, ns in recs)
+
+
+def test_met_replication_between_devices(rt):
+    """A snapshot one device holds reaches another by GPU-to-GPU copy
+    (lt_met_copy_slot), not a second host upload; values identical."""
+    dr, _, _, ms, syn = rt
+    from paper_2211_12616_b200.context import DeviceContext
+    m0, m1 = syn.analytic_pair(dlon=10.0, dlat=5.0, nlev=16)
+    a, b = DeviceContext(0), DeviceContext(0)
+    a.bind_pair(m0, m1)
+    loads = []
+    orig = b.load_met
+    b.load_met = lambda *args, **kw: (loads.append(args), orig(*args, **kw))
+    b.bind_pair(m0, m1, donor=lambda key: (a, a.find_slot(key)) if a.find_slot(key) is not None
+                else None)
+    assert loads == []
+    rs = np.random.default_rng(2)
+    lon, lat, p = rs.uniform(-180, 180, 5000), rs.uniform(-90, 90, 5000), rs.uniform(5, 1000, 5000)
+    np.testing.assert_array_equal(b.interpolate(1800.0, lon, lat, p),
+                                  a.interpolate(1800.0, lon, lat, p))
+    a.close()
+    b.close()
+    # the pool wires the donor in: the second device's image copies from the first
+    host = dr.ModelImage(ctl=ms.Control(), ens=syn.particles(10), cache=ms.cache_allocate(10),
+                         clim=ms.read_clim(), met0=m0, met1=m1, dt=np.zeros(10), batch=None)
+    with dr.DevicePool(2) as pool:
+        r0 = pool.region_create(0, host, None, with_batch=False)
+        pool.region_update_device(r0, host, ("met0", "met1"))
+        r1 = pool.region_create(1, host, None, with_batch=False)
+        c1 = r1.image.engine.ctx
+        seen = []
+        orig1 = c1.copy_slot_from
+        c1.copy_slot_from = lambda *args, **kw: (seen.append(args), orig1(*args, **kw))
+        pool.region_update_device(r1, host, ("met0", "met1"))
+        assert len(seen) == 2
