@@ -23,7 +23,10 @@ static cudaError_t launch_fixed(const StepArgs<Rec>& a, cudaStream_t st) {
   const int64_t n = a.end - a.start;
   if (n <= 0) return cudaSuccess;
   int64_t grid = (n + 255) / 256;
-  const int64_t cap = static_cast<int64_t>(sms) * blocks_per_sm * 16;
+#ifndef LT_GRID_WAVES
+#define LT_GRID_WAVES 16
+#endif
+  const int64_t cap = static_cast<int64_t>(sms) * blocks_per_sm * LT_GRID_WAVES;
   if (grid > cap) grid = cap;
   step_kernel<Rec, FIXED, FAST, RM><<<static_cast<unsigned>(grid), 256, 0, st>>>(a);
   return cudaGetLastError();

@@ -130,15 +130,20 @@ __global__ void __launch_bounds__(256, LT_STEP_MIN_BLOCKS) step_kernel(const Ste
   using O = Ops<Rec, FAST>;
   const uint32_t mods = FIXED ? FIXED : a.modules;
   const Control& ctl = a.ctl;
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  // each block walks its own contiguous run of (box-sorted) particles tile
+  // by tile, so consecutive tiles reuse the met records left in L1
+  const int64_t ntile = (a.end - a.start + blockDim.x - 1) / blockDim.x;
+  const int64_t per = (ntile + gridDim.x - 1) / gridDim.x;
+  const int64_t s_lo = a.start + static_cast<int64_t>(blockIdx.x) * per * blockDim.x;
+  const int64_t s_hi = min(a.end, s_lo + per * blockDim.x);
+  const int64_t stride = blockDim.x;
   unsigned long long nonconv = 0;
 
-  for (int64_t s = a.start + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-       s < a.end; s += stride) {
+  for (int64_t s = s_lo + threadIdx.x; s < s_hi; s += stride) {
     // stage the next particle's state rows into L2 while this one runs
     // (costs no registers; the loads below then hit L2 instead of HBM)
 #ifndef LT_NO_PREFETCH
-    if (s + stride < a.end) {
+    if (s + stride < s_hi) {
       const int64_t nx = s + stride;
       prefetch_l2(a.time + nx); prefetch_l2(a.lon + nx); prefetch_l2(a.lat + nx);
       prefetch_l2(a.p + nx);
