@@ -326,6 +326,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=("b200", "reference"))
     ap.add_argument("--sort-every", type=int, default=-1)
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-chunk", type=int, default=0,
+                    help="particles per host-path chunk (0: the library default)")
     ap.add_argument("--alt-steps", type=int, default=-1,
                     help="timed steps with the other precision's kernels (default: --steps)")
     ap.add_argument("--cpu-sample", type=int, default=0)
@@ -475,12 +477,12 @@ def main():
         hcache.uvwp[:] = 0.0
         if want_iso:
             eng.ctx.d2h_ordered(capi.F_ISO_VAR, 0, 0, n, eng.first_id, out=hcache.iso_var)
-        eng.step_host(ctl, hens, hcache, step, mask)   # warm-up (allocations, events)
+        eng.step_host(ctl, hens, hcache, step, mask, chunk=args.e2e_chunk)   # warm-up
         step += 1
         barrier()
         t0 = time.perf_counter()
         for k in range(args.e2e_steps):
-            eng.step_host(ctl, hens, hcache, step, mask)
+            eng.step_host(ctl, hens, hcache, step, mask, chunk=args.e2e_chunk)
             step += 1
         barrier()
         te = sharding.max_over_ranks([time.perf_counter() - t0], dist, "cuda")[0]
