@@ -348,16 +348,23 @@ def main():
 
     cfg = WORKLOADS[wl]
     ws, rank, local = dist_env()
-    torch.cuda.set_device(local)
+    # one rank per GPU; LT_DIST_BACKEND=gloo with more ranks than GPUs maps
+    # ranks round-robin onto the GPUs present (tests the N > 1 path on one GPU)
+    gpu = local % torch.cuda.device_count()
+    torch.cuda.set_device(gpu)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("LT_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", gpu))
+        else:
+            dist.init_process_group(backend)
     n_tot = cfg["n"]
     mask = engine.modules_mask(cfg["chain"])
     work = sharding.shard_range(n_tot, ws, rank)
     ctl = make_ctl(wl, args.precision)
 
     mets = build_met(wl, rank, ws)
-    eng = engine.Engine(device=local, first_id=work.start, met_precision=args.met_store,
+    eng = engine.Engine(device=gpu, first_id=work.start, met_precision=args.met_store,
                         nq=ctl.nq)
     ens = make_particles(wl, work.size, 12616 + rank)
     eng.upload(ens)
@@ -423,7 +430,7 @@ def main():
         sorts0 = n_sorts
         rot0 = stream["rotations"] if stream else 0
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * k_steps + 2)]
-        with ClockSampler(local) as clk:
+        with ClockSampler(gpu) as clk:
             ev[0].record(stream_h)
             for k in range(k_steps):
                 one_step(c, (ev[2 + 2 * k], ev[3 + 2 * k]))
