@@ -17,18 +17,18 @@ static cudaError_t launch_fixed(const StepArgs<Rec>& a, cudaStream_t st) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, step_kernel<Rec, FIXED, FAST, RM>, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, step_kernel<Rec, FIXED, FAST, RM>, LT_STEP_BLOCK, 0);
     if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
   const int64_t n = a.end - a.start;
   if (n <= 0) return cudaSuccess;
-  int64_t grid = (n + 255) / 256;
+  int64_t grid = (n + LT_STEP_BLOCK - 1) / LT_STEP_BLOCK;
 #ifndef LT_GRID_WAVES
 #define LT_GRID_WAVES 16
 #endif
   const int64_t cap = static_cast<int64_t>(sms) * blocks_per_sm * LT_GRID_WAVES;
   if (grid > cap) grid = cap;
-  step_kernel<Rec, FIXED, FAST, RM><<<static_cast<unsigned>(grid), 256, 0, st>>>(a);
+  step_kernel<Rec, FIXED, FAST, RM><<<static_cast<unsigned>(grid), LT_STEP_BLOCK, 0, st>>>(a);
   return cudaGetLastError();
 }
 

@@ -44,12 +44,25 @@ __device__ __forceinline__ void prefetch_l2(const void* ptr) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
 }
 
+// particle-state rows are touched once per step: stream them past L1
+// (evict-first) so L1 keeps the met records the gathers reuse
+#ifndef LT_NO_STREAM_STATE
+__device__ __forceinline__ double ld_state(const double* p) { return __ldcs(p); }
+__device__ __forceinline__ void st_state(double* p, double v) { __stcs(p, v); }
+#else
+__device__ __forceinline__ double ld_state(const double* p) { return *p; }
+__device__ __forceinline__ void st_state(double* p, double v) { *p = v; }
+#endif
+
 __device__ __forceinline__ void prefetch_l1(const void* ptr) {
   asm volatile("prefetch.global.L1 [%0];" ::"l"(ptr));
 }
 
+#ifndef LT_STEP_BLOCK
+#define LT_STEP_BLOCK 256
+#endif
 #ifndef LT_STEP_MIN_BLOCKS
-#define LT_STEP_MIN_BLOCKS 4
+#define LT_STEP_MIN_BLOCKS (1024 / LT_STEP_BLOCK)
 #endif
 
 // Arithmetic policy: EXACT reproduces numpy's operation sequence in fp64;
@@ -126,7 +139,7 @@ __device__ __forceinline__ void draws(const StepArgs<Rec>& a, int64_t s, uint64_
 }
 
 template <class Rec, uint32_t FIXED, bool FAST, int RM>
-__global__ void __launch_bounds__(256, LT_STEP_MIN_BLOCKS) step_kernel(const StepArgs<Rec> a) {
+__global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel(const StepArgs<Rec> a) {
   using O = Ops<Rec, FAST>;
   const uint32_t mods = FIXED ? FIXED : a.modules;
   const Control& ctl = a.ctl;
@@ -158,7 +171,8 @@ __global__ void __launch_bounds__(256, LT_STEP_MIN_BLOCKS) step_kernel(const Ste
       prefetch_l1(a.uvwp[0] + s); prefetch_l1(a.uvwp[1] + s); prefetch_l1(a.uvwp[2] + s);
     }
 #endif
-    double time = a.time[s], lon = a.lon[s], lat = a.lat[s], p = a.p[s];
+    double time = ld_state(a.time + s), lon = ld_state(a.lon + s), lat = ld_state(a.lat + s),
+           p = ld_state(a.p + s);
 
     // physics.py:82-88 (module_timesteps)
     double dt;
@@ -240,7 +254,7 @@ __global__ void __launch_bounds__(256, LT_STEP_MIN_BLOCKS) step_kernel(const Ste
       // their latency overlaps that work
       double up[3];
 #pragma unroll
-      for (int f = 0; f < 3; ++f) up[f] = a.uvwp[f][s];
+      for (int f = 0; f < 3; ++f) up[f] = ld_state(a.uvwp[f] + s);
 #endif
       double xm[3];
       draws<O, RM>(a, s, gid, 2, xm);
@@ -256,9 +270,9 @@ __global__ void __launch_bounds__(256, LT_STEP_MIN_BLOCKS) step_kernel(const Ste
 #ifdef LT_MESO_EARLY
         pert[f] = r * up[f] + amp * sigma * xm[f];
 #else
-        pert[f] = r * a.uvwp[f][s] + amp * sigma * xm[f];
+        pert[f] = r * ld_state(a.uvwp[f] + s) + amp * sigma * xm[f];
 #endif
-        a.uvwp[f][s] = pert[f];
+        st_state(a.uvwp[f] + s, pert[f]);
       }
       const double nlon = lon + O::over_cos(pert[0] * dt * kDegPerM, lat);
       lat = lat + pert[1] * dt * kDegPerM;
@@ -340,10 +354,10 @@ __global__ void __launch_bounds__(256, LT_STEP_MIN_BLOCKS) step_kernel(const Ste
     }
 
     if (mods & (M_ADVECTION | M_TURB | M_MESO | M_CONVECTION | M_SEDI | M_ISOSURF | M_POSITION)) {
-      a.p[s] = p;
-      a.lon[s] = lon;
-      a.lat[s] = lat;
-      if (mods & M_ADVECTION) a.time[s] = time;
+      st_state(a.p + s, p);
+      st_state(a.lon + s, lon);
+      st_state(a.lat + s, lat);
+      if (mods & M_ADVECTION) st_state(a.time + s, time);
     }
   }
 
