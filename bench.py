@@ -9,8 +9,9 @@ quoted on): **cfg3** — 1e8 particles on the synthetic ERA5-like 0.25 deg grid
 (+ timesteps, in-kernel counter RNG, position), sharded over N GPUs with the
 reference partition rule, met replicated to every rank by an NCCL
 broadcast.  A "step" is one fused time step of every particle; the box sort
-runs every `--sort-every` steps (20 for cfg3, the measured optimum of
-5/10/20/40) inside the timed region.
+runs every `--sort-every` steps (15 for cfg3, the measured optimum of
+8/10/15/20; the default 30 timed steps hold exactly two sorts) inside the
+timed region.
 
 Other workloads (parity shapes, informational lines): cfg1 (SBR, 1e5,
 advection), cfg2 (1e7, 1 deg), cfg4 (5e7 volcanic point release, advection
@@ -61,7 +62,7 @@ WORKLOADS = {
                  init="uniform", sort_every=10,
                  desc="1e7 particles, ERA5-like 1deg 360x181x60, advection+turb+meso diffusion"),
     "cfg3": dict(n=100_000_000, grid=(0.25, 0.25, 137, 0.01), met="era5", chain=ADV_DIFF,
-                 init="uniform", sort_every=20,
+                 init="uniform", sort_every=15,
                  desc="1e8 particles, ERA5-like 0.25deg 1440x721x137, advection+turb+meso "
                       "diffusion"),
     "cfg4": dict(n=50_000_000, grid=(0.25, 0.25, 137, 0.01), met="stream", chain=PLUME,
@@ -320,7 +321,7 @@ def run_reference(args, wl):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="cfg3", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="b200", choices=("b200", "reference"))

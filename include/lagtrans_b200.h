@@ -193,6 +193,16 @@ int lt_interpolate(lt_ctx *ctx, int64_t n, const double *t, const double *lon,
 /* theta-isosurface non-convergence counter (CacheState.iso_nonconverged) */
 int lt_iso_counter(lt_ctx *ctx, int64_t *value, int32_t reset);
 
+/* Row groups that may stay in particle ("home") order while the store is
+   box-sorted: the element of global particle id g sits at index
+   g - home_base (home_base = first_id of the last lt_ids_reset, which must
+   start at offset 0), so the sort need not move them; kernels reach them
+   through the id row.  lt_set_home_rows converts the current layout. */
+#define LT_HOME_Q    (1u << 0)
+#define LT_HOME_ZETA (1u << 1)
+#define LT_HOME_DT   (1u << 2)
+int lt_set_home_rows(lt_ctx *ctx, uint32_t mask);
+
 /* box sort: stable radix sort of [start, end) by met0 cell, ids travel along */
 int lt_sort_by_box(lt_ctx *ctx, int64_t start, int64_t end);
 /* copies that undo the sort permutation (ids must be a permutation of

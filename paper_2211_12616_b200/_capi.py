@@ -42,6 +42,8 @@ PRECISIONS = {"exact": 0, "fast": 1}
 F_TIME, F_P, F_ZETA, F_LON, F_LAT, F_Q, F_UVWP, F_ISO_VAR, F_DT = range(9)
 F_RND_CONV, F_RND_TURB, F_RND_MESO, F_ID = 9, 10, 11, 12
 
+HOME_Q, HOME_ZETA, HOME_DT = 1, 2, 4
+
 MET_F32, MET_F64 = 4, 8
 MET_CLOSE_LON = 1
 MET_DEVICE_SRC = 2
@@ -119,6 +121,7 @@ _PROTOS = {
     "lt_rng_fill": ([_P, _I32, _U64, _I64, _I64, _I64], C.c_int),
     "lt_iso_counter": ([_P, C.POINTER(_I64), _I32], C.c_int),
     "lt_sort_by_box": ([_P, _I64, _I64], C.c_int),
+    "lt_set_home_rows": ([_P, _U32], C.c_int),
     "lt_field_d2h_ordered": ([_P, _I32, _I32, _I64, _I64, _I64, _P], C.c_int),
     "lt_field_h2d_ordered": ([_P, _I32, _I32, _I64, _I64, _I64, _P], C.c_int),
     "lt_timing": ([_P, _I32], C.c_int),

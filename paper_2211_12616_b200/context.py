@@ -273,6 +273,10 @@ class DeviceContext:
         capi.check(self.lib.lt_iso_counter(self.h, C.byref(v), int(reset)))
         return int(v.value)
 
+    def set_home_rows(self, mask: int) -> None:
+        """Keep the HOME_* row groups in particle order (not moved by sorts)."""
+        capi.check(self.lib.lt_set_home_rows(self.h, mask))
+
     def sort_by_box(self, start: int, end: int) -> None:
         capi.check(self.lib.lt_sort_by_box(self.h, start, end))
 

@@ -78,6 +78,9 @@ struct lt_ctx {
   double* uvwp[3] = {nullptr, nullptr, nullptr};  // separate rows: the sort swaps row pointers
   double *rnd_conv = nullptr, *rnd_turb = nullptr, *rnd_meso = nullptr;
   uint32_t* ids = nullptr;
+  uint32_t home_mask = 0;        // LT_HOME_* row groups kept in particle order
+  int64_t home_base = 0;         // first id of the last lt_ids_reset (offset 0)
+  int64_t home_n = 0;            // particles [0, home_n) carry home-order ids
   double* scratch = nullptr;     // cap doubles (ordered copies)
   double* pool[kRowSet] = {};    // cap doubles each: sort gather targets (swapped with rows)
   uint32_t* sort_buf = nullptr;  // 4 * cap (keys in/out, vals in/out)
@@ -310,6 +313,7 @@ static void free_particles(lt_ctx* c) {
     *p = nullptr;
   }
   free_dev(c->ids); c->ids = nullptr;
+  c->home_mask = 0; c->home_base = 0; c->home_n = 0;
   for (double*& r : c->pool) { free_dev(r); r = nullptr; }
   free_dev(c->sort_buf); c->sort_buf = nullptr;
   free_dev(c->cub_temp); c->cub_temp = nullptr; c->cub_bytes = 0;
@@ -471,6 +475,53 @@ int lt_ids_reset(lt_ctx* c, int64_t off, int64_t cnt, int64_t first_id) {
   if (first_id < 0 || first_id + cnt > (int64_t(1) << 32))
     return fail(LT_ERR_ARG, "particle ids must fit in 32 bits");
   CK(launch_iota(c->ids, off, cnt, first_id, c->stream));
+  if (off == 0) {   // slot s now holds particle first_id + s: home order == slot order
+    c->home_base = first_id;
+    c->home_n = cnt;
+  }
+  return LT_OK;
+}
+
+// Convert row groups between slot order and particle ("home") order.  With
+// ids a permutation of [home_base, home_base + home_n) over slots
+// [0, home_n): slot -> home scatters out[id - base] = in[s]; home -> slot
+// gathers out[s] = in[id - base].
+static int convert_row(lt_ctx* c, double** row, bool separate, bool to_home) {
+  const int64_t n = c->home_n;
+  if (n == 0 || !c->ids) return LT_OK;
+  if (int rc = ensure_pool(c)) return rc;
+  CK(cudaMemsetAsync(c->bad, 0, sizeof(int), c->stream));
+  double* tmp = c->pool[0];
+  if (to_home) CK(launch_unsort(tmp, *row, c->ids, 0, n, c->home_base, c->bad, 1, c->stream));
+  else CK(launch_resort(tmp, *row, c->ids, 0, n, c->home_base, c->bad, 1, c->stream));
+  if (separate && n == c->cap) std::swap(*row, c->pool[0]);
+  else CK(cudaMemcpyAsync(*row, tmp, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+  return LT_OK;
+}
+
+int lt_set_home_rows(lt_ctx* c, uint32_t mask) {
+  int rc = check_ctx(c);
+  if (rc || (rc = check_particles(c))) return rc;
+  if (mask & ~(LT_HOME_Q | LT_HOME_ZETA | LT_HOME_DT)) return fail(LT_ERR_ARG, "unknown home row bits");
+  const uint32_t change = mask ^ c->home_mask;
+  if (!change) return LT_OK;
+  if (c->ids && c->home_n == 0)
+    return fail(LT_ERR_STATE, "home order needs an id layout from lt_ids_reset at offset 0");
+  if (change & LT_HOME_ZETA)
+    if ((rc = convert_row(c, &c->zeta, true, mask & LT_HOME_ZETA))) return rc;
+  if (change & LT_HOME_DT)
+    if ((rc = convert_row(c, &c->dt, true, mask & LT_HOME_DT))) return rc;
+  if (change & LT_HOME_Q)
+    for (int k = 0; k < c->nq; ++k) {
+      double* r = c->q + static_cast<int64_t>(k) * c->cap;
+      if ((rc = convert_row(c, &r, false, mask & LT_HOME_Q))) return rc;
+    }
+  int bad = 0;
+  CK(cudaMemcpyAsync(&bad, c->bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (bad) return fail(LT_ERR_STATE, "particle ids of [0, %lld) are not a permutation of the home range",
+                       (long long)c->home_n);
+  c->home_mask = mask;
   return LT_OK;
 }
 
@@ -669,6 +720,8 @@ static int run_typed(lt_ctx* c, const lt_control* ctl, uint32_t modules, int64_t
   for (int k = 0; k < 3; ++k) a.uvwp[k] = c->uvwp[k];
   a.iso_var = c->iso_var; a.q = c->q;
   a.ids = c->ids;
+  a.home_mask = c->home_mask;
+  a.home_base = c->home_base;
   a.rnd_conv = c->rnd_conv; a.rnd_turb = c->rnd_turb; a.rnd_meso = c->rnd_meso;
   a.cap = c->cap; a.start = start; a.end = end; a.nq = c->nq;
   a.modules = modules; a.flags = flags; a.step = step;
@@ -750,6 +803,9 @@ int lt_run_host(lt_ctx* c, const lt_control* ctl, uint32_t modules, int64_t n, i
   if (decay && (ctl->decay_slot >= io->nq || ctl->decay_slot >= c->nq))
     return fail(LT_ERR_ARG, "decay_slot outside the q rows");
   if (n == 0) return LT_OK;
+  // the store is scratch for this call: every row in slot order
+  c->home_mask = 0;
+  c->home_n = 0;
   if (chunk <= 0) chunk = std::min<int64_t>(c->cap, std::max<int64_t>(int64_t(1) << 20, (n + 15) / 16));
   chunk = std::min(chunk, c->cap);
   if (chunk <= 0) return fail(LT_ERR_STATE, "particle store has no capacity");
@@ -903,8 +959,10 @@ static int sort_typed(lt_ctx* c, int64_t start, int64_t end) {
   // the gathered slice back.
   if (int rc = ensure_pool(c)) return rc;
   const bool whole = start == 0 && end == c->cap;
-  std::vector<double**> rows = {&c->time, &c->p, &c->zeta, &c->lon, &c->lat, &c->iso_var, &c->dt,
+  std::vector<double**> rows = {&c->time, &c->p, &c->lon, &c->lat, &c->iso_var,
                                 &c->uvwp[0], &c->uvwp[1], &c->uvwp[2]};
+  if (!(c->home_mask & LT_HOME_ZETA)) rows.push_back(&c->zeta);
+  if (!(c->home_mask & LT_HOME_DT)) rows.push_back(&c->dt);
   for (size_t g = 0; g < rows.size(); g += kRowSet) {
     RowSet rs;
     rs.n = static_cast<int>(std::min<size_t>(kRowSet, rows.size() - g));
@@ -915,7 +973,7 @@ static int sort_typed(lt_ctx* c, int64_t start, int64_t end) {
       else CK(cudaMemcpyAsync(*rows[g + k] + start, c->pool[k] + start, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
     }
   }
-  for (int g = 0; g < c->nq; g += kRowSet) {
+  for (int g = 0; g < ((c->home_mask & LT_HOME_Q) ? 0 : c->nq); g += kRowSet) {
     RowSet rs;
     rs.n = std::min(kRowSet, c->nq - g);
     for (int k = 0; k < rs.n; ++k) { rs.src[k] = c->q + static_cast<int64_t>(g + k) * c->cap; rs.dst[k] = c->pool[k]; }
@@ -942,6 +1000,9 @@ int lt_sort_by_box(lt_ctx* c, int64_t start, int64_t end) {
       (rc = alloc_dev(reinterpret_cast<void**>(&c->sort_buf), 4 * sizeof(uint32_t) * c->cap, "sort keys")))
     return rc;
   if (end == start) return LT_OK;
+  if (c->home_mask && end > c->home_n)
+    return fail(LT_ERR_RANGE, "sort range [%lld, %lld) exceeds the home-order id range [0, %lld)",
+                (long long)start, (long long)end, (long long)c->home_n);
   if (c->timing) CK(cudaEventRecord(c->ev_start, c->stream));
   rc = c->prec == LT_MET_F64 ? sort_typed<RecD>(c, start, end) : sort_typed<RecF>(c, start, end);
   if (rc) return rc;
@@ -963,6 +1024,14 @@ static int ordered_copy(lt_ctx* c, int32_t field, int32_t row, int64_t off, int6
   if (!c->ids) {  // never sorted: plain copy
     return to_host ? lt_field_d2h(c, field, row, off, cnt, host)
                    : lt_field_h2d(c, field, row, off, cnt, host);
+  }
+  const uint32_t group = field == LT_F_Q ? LT_HOME_Q : field == LT_F_ZETA ? LT_HOME_ZETA
+                         : field == LT_F_DT ? LT_HOME_DT : 0u;
+  if (group & c->home_mask) {  // particle order already: contiguous at id - home_base
+    const int64_t at = first_id - c->home_base;
+    if ((rc = slice_check(c, at, cnt, len))) return rc;
+    return to_host ? lt_field_d2h(c, field, row, at, cnt, host)
+                   : lt_field_h2d(c, field, row, at, cnt, host);
   }
   if ((rc = ensure_scratch(c))) return rc;
   if (cnt == 0) return LT_OK;
@@ -1036,13 +1105,14 @@ int lt_group_stats(lt_ctx* c, int32_t slot, int64_t start, int64_t end, int64_t 
   int64_t ng = 0;
   std::vector<uint32_t> g32(std::max<int64_t>(max_groups, 1));
   std::vector<double> m(3 * std::max<int64_t>(max_groups, 1)), sd(m.size());
-  CK(group_stats(c->lon, c->lat, c->p, qrow, c->ids, start, n, max_groups, nullptr, 0, &need,
+  const int64_t qbase = (c->home_mask & LT_HOME_Q) && c->ids ? c->home_base : -1;
+  CK(group_stats(c->lon, c->lat, c->p, qrow, c->ids, qbase, start, n, max_groups, nullptr, 0, &need,
                  c->bad, &ng, g32.data(), count, m.data(), sd.data(), c->stream));
   void* ws = nullptr;
   if ((rc = alloc_dev(&ws, need, "group stats workspace"))) return rc;
   cudaError_t e = cudaMemsetAsync(c->bad, 0, sizeof(int), c->stream);
   if (e == cudaSuccess)
-    e = group_stats(c->lon, c->lat, c->p, qrow, c->ids, start, n, max_groups, ws, need, &need,
+    e = group_stats(c->lon, c->lat, c->p, qrow, c->ids, qbase, start, n, max_groups, ws, need, &need,
                     c->bad, &ng, g32.data(), count, m.data(), sd.data(), c->stream);
   int bad = 0;
   if (e == cudaSuccess) e = cudaMemcpy(&bad, c->bad, sizeof(int), cudaMemcpyDeviceToHost);

@@ -57,7 +57,7 @@ cudaError_t launch_grid_counts(const double* lon, const double* lat, int64_t sta
                                int nx, int ny, unsigned long long* counts, int sms,
                                cudaStream_t st);
 cudaError_t group_stats(const double* lon, const double* lat, const double* p, const double* qrow,
-                        const uint32_t* ids, int64_t start, int64_t n, int64_t max_groups, void* ws,
+                        const uint32_t* ids, int64_t qbase, int64_t start, int64_t n, int64_t max_groups, void* ws,
                         size_t ws_bytes, size_t* ws_need, int* bad_dev, int64_t* ngroups_out,
                         uint32_t* gid_out, int64_t* count_out, double* mean_out, double* std_out,
                         cudaStream_t st);

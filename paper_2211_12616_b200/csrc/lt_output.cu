@@ -78,11 +78,14 @@ cudaError_t launch_grid_counts(const double* lon, const double* lat, int64_t sta
 
 // key = (group id << 32) | particle id: groups ascending, and inside a group
 // particles in id order whatever the store's (box-sorted) slot order
-__global__ void group_keys_kernel(const double* qrow, const uint32_t* ids, int64_t start, int64_t n,
-                                  uint64_t* keys, uint32_t* vals, int* bad) {
+__global__ void group_keys_kernel(const double* qrow, const uint32_t* ids, int64_t qbase,
+                                  int64_t start, int64_t n, uint64_t* keys, uint32_t* vals,
+                                  int* bad) {
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const double g = trunc(qrow[start + t]);
+    // qbase >= 0: the q rows are in particle (home) order
+    const int64_t qi = qbase >= 0 ? static_cast<int64_t>(ids[start + t]) - qbase : start + t;
+    const double g = trunc(qrow[qi]);
     uint64_t gid = 0;
     if (!(g >= 0.0)) *bad = 1;
     else if (g > 4294967295.0) *bad = 2;
@@ -144,7 +147,7 @@ static int grid_n(int64_t n) {
 // ws = null for the size).  *ngroups_out > max_groups means the result
 // arrays were too small and nothing was written.
 cudaError_t group_stats(const double* lon, const double* lat, const double* p, const double* qrow,
-                        const uint32_t* ids, int64_t start, int64_t n, int64_t max_groups, void* ws, size_t ws_bytes,
+                        const uint32_t* ids, int64_t qbase, int64_t start, int64_t n, int64_t max_groups, void* ws, size_t ws_bytes,
                         size_t* ws_need, int* bad_dev, int64_t* ngroups_out, uint32_t* gid_out,
                         int64_t* count_out, double* mean_out, double* std_out, cudaStream_t st) {
   // layout: keys_in, keys_out (u64 n) | vals_in, vals_out, gids (u32 n) | fields 3n f64 |
@@ -199,7 +202,7 @@ cudaError_t group_stats(const double* lon, const double* lat, const double* p, c
   size_t tb = t_need;
   cudaError_t e;
 
-  group_keys_kernel<<<grid_n(n), 256, 0, st>>>(qrow, ids, start, n, keys_in, vals_in, bad_dev);
+  group_keys_kernel<<<grid_n(n), 256, 0, st>>>(qrow, ids, qbase, start, n, keys_in, vals_in, bad_dev);
   if ((e = cub::DeviceRadixSort::SortPairs(tmp, tb, keys_in, keys_out, vals_in, vals_out,
                                            static_cast<int>(n), 0, 64, st))) return e;
   high_words_kernel<<<grid_n(n), 256, 0, st>>>(keys_out, n, gids);

@@ -25,6 +25,8 @@ struct StepArgs {
   double* iso_var;
   double* q;
   const uint32_t* ids;  // global particle index per slot, or null (= slot)
+  uint32_t home_mask;   // HOME_* row groups kept in particle order (index id - home_base)
+  int64_t home_base;
   const double* rnd_conv;
   const double* rnd_turb;
   const double* rnd_meso;
@@ -138,6 +140,12 @@ __device__ __forceinline__ void draws(const StepArgs<Rec>& a, int64_t s, uint64_
   }
 }
 
+// index of slot s in a row group that may be kept in particle order
+template <class Rec>
+__device__ __forceinline__ int64_t row_index(const StepArgs<Rec>& a, int64_t s, uint32_t group) {
+  return (a.home_mask & group) && a.ids ? static_cast<int64_t>(a.ids[s]) - a.home_base : s;
+}
+
 template <class Rec, uint32_t FIXED, bool FAST, int RM>
 __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel(const StepArgs<Rec> a) {
   using O = Ops<Rec, FAST>;
@@ -179,9 +187,9 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
     if ((mods & M_TIMESTEPS) || !(a.flags & F_DT_ARRAY)) {
       dt = fmin(ctl.dt_model, ctl.t_stop - time);
       dt = fmin(fmax(dt, 0.0), ctl.dt_model);
-      if ((mods & M_TIMESTEPS) && (a.flags & F_WRITE_DT)) a.dt[s] = dt;
+      if ((mods & M_TIMESTEPS) && (a.flags & F_WRITE_DT)) a.dt[row_index(a, s, HOME_DT)] = dt;
     } else {
-      dt = a.dt[s];
+      dt = a.dt[row_index(a, s, HOME_DT)];
     }
     const bool act = dt > 0.0;
 
@@ -301,7 +309,7 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
     // decay (new module): q[slot] *= exp(-dt / tau) while active
     if ((mods & M_DECAY) && ctl.decay_tau > 0.0 && act && ctl.decay_slot >= 0 &&
         ctl.decay_slot < a.nq) {
-      double* qs = a.q + static_cast<int64_t>(ctl.decay_slot) * a.cap + s;
+      double* qs = a.q + static_cast<int64_t>(ctl.decay_slot) * a.cap + row_index(a, s, HOME_Q);
       *qs = *qs * exp(-dt / ctl.decay_tau);
     }
 
@@ -346,11 +354,12 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
     if (mods & M_METEO) {
       double v[4];
       O::sample(a.met, time, lon, lat, p, 11, v);
-      a.q[s] = v[3];
-      a.q[a.cap + s] = v[0];
-      a.q[2 * a.cap + s] = v[1];
-      a.q[3 * a.cap + s] = clim_hno3(a.clim, lat, p);
-      a.q[4 * a.cap + s] = p < clim_ptrop(a.clim, lat) ? 1.0 : 0.0;
+      const int64_t qi = row_index(a, s, HOME_Q);
+      a.q[qi] = v[3];
+      a.q[a.cap + qi] = v[0];
+      a.q[2 * a.cap + qi] = v[1];
+      a.q[3 * a.cap + qi] = clim_hno3(a.clim, lat, p);
+      a.q[4 * a.cap + qi] = p < clim_ptrop(a.clim, lat) ? 1.0 : 0.0;
     }
 
     if (mods & (M_ADVECTION | M_TURB | M_MESO | M_CONVECTION | M_SEDI | M_ISOSURF | M_POSITION)) {

@@ -178,6 +178,7 @@ class Engine:
             self.faithful_state = advance_faithful(fstate, self.n)
         self.ctx.run(ctl, modules, 0, self.n, step=step, faithful_state=fstate,
                      faithful_base=self.first_id, flags=capi.RUN_RNG_INKERNEL)
+        self._last_modules = modules
 
     def step_host(self, ctl, ens, cache, step: int, modules: int = ADV_DIFF,
                   device_id: int = 0, chunk: int = 0) -> None:
@@ -204,6 +205,13 @@ class Engine:
         self.sorted = False
 
     def sort(self) -> None:
+        """Stable box sort of the shard.  Rows the stepping modules do not
+        touch (zeta, dt, and q unless meteo/decay run) stay in particle
+        order, so the sort moves only the rows the step kernel streams."""
+        home = capi.HOME_ZETA | capi.HOME_DT
+        if not (getattr(self, "_last_modules", 0) & (capi.MOD_METEO | capi.MOD_DECAY)):
+            home |= capi.HOME_Q   # (a later meteo/decay step still works, via the ids)
+        self.ctx.set_home_rows(home)
         self.ctx.sort_by_box(0, self.n)
         self.sorted = True
 

@@ -227,3 +227,78 @@ def test_host_path_equals_device_path_bitwise(eng, golden_chain, chunk):
     np.testing.assert_array_equal(host.q, ref.q)
     np.testing.assert_array_equal(cache.uvwp, rc.uvwp)
     np.testing.assert_array_equal(cache.iso_var, rc.iso_var)
+
+
+def test_home_order_rows_follow_particles(eng, golden_chain):
+    """Rows the chain does not touch stay in particle order through sorts
+    (lt_set_home_rows); downloads, statistics and a later switch to a chain
+    that writes q (meteo) see the same particles as an unsorted run."""
+    engine, ms, _ = eng
+    g = golden_chain
+    m0, m1 = snapshot_from(g, "m0"), snapshot_from(g, "m1")
+    ctl = chain_ctl()
+    base = _ens(ms, g, "init")
+    n = base.np
+    base.zeta[:] = np.arange(n) * 0.5
+    q = np.zeros((6, n))
+    q[5] = np.arange(n) % 7
+    base = ms.ParticleEnsemble(n, base.time, base.p, base.zeta, base.lon, base.lat, q)
+
+    def run(sort_every):
+        e = engine.Engine(device=0, nq=6, first_id=0)
+        e.upload(base)
+        e.bind_met(m0, m1)
+        e.load_clim(ms.read_clim(ctl))
+        e.init_isosurf(ctl)
+        for step in range(6):
+            if sort_every and step % sort_every == 0:
+                e.sort()
+            e.step(ctl, step, engine.ADV_DIFF)
+        mid = e.download()
+        for step in range(6, 10):
+            if sort_every and step % sort_every == 0:
+                e.sort()
+            e.step(ctl, step, engine.FULL)
+        out = e.download()
+        e.close()
+        return mid, out
+
+    mid0, out0 = run(0)
+    mid2, out2 = run(2)
+    np.testing.assert_array_equal(mid2.zeta, base.zeta)
+    np.testing.assert_array_equal(mid2.q, base.q)
+    for k in ("lon", "lat", "p", "time"):
+        np.testing.assert_array_equal(getattr(mid2, k), getattr(mid0, k))
+        np.testing.assert_array_equal(getattr(out2, k), getattr(out0, k))
+    np.testing.assert_array_equal(out2.q, out0.q)
+    np.testing.assert_array_equal(out2.zeta, base.zeta)
+
+
+def test_group_stats_with_home_order_q(eng):
+    engine, ms, syn = eng
+    from paper_2211_12616_b200 import output
+    from paper_2211_12616_b200.device_runtime import DevicePool, ModelImage
+    m0, m1 = syn.analytic_pair(dlon=10.0, dlat=5.0, nlev=12)
+    ens = syn.particles(20000, seed=4, nq=6)
+    ens.q[5] = np.arange(ens.np) % 5
+    ctl = ms.Control(ens_group_slot=5, nq=6, rng_mode="counter")
+    host = ModelImage(ctl=ctl, ens=ens, cache=ms.cache_allocate(ens.np), clim=ms.read_clim(),
+                      met0=m0, met1=m1, dt=np.zeros(ens.np), batch=None)
+    with DevicePool(1) as pool:
+        r = pool.region_create(0, host, None, with_batch=False)
+        pool.region_update_device(r, host, ("ens", "met0", "met1"))
+        before = output.group_stats(ctl, r.image.ens)
+        img = r.image
+
+        def go():
+            img.engine.step(ctl, 0, engine.ADV_DIFF)
+            img.engine.sort()       # q now kept in particle order
+        pool.dispatch(0, go).result()
+        after = output.group_stats(ctl, r.image.ens)
+        back = img.engine.download()
+    np.testing.assert_array_equal(back.q[5], ens.q[5])
+    og, oc, om, osd = orc.grouped_moments(back.q[5], back.lon, back.lat, back.p)
+    np.testing.assert_array_equal(after[0], og)
+    np.testing.assert_array_equal(after[1], oc)
+    np.testing.assert_allclose(after[2], om, rtol=1e-12)
+    np.testing.assert_array_equal(before[1], after[1])
