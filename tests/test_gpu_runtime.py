@@ -195,3 +195,23 @@ def test_met_replication_between_devices(rt):
         c1.copy_slot_from = lambda *args, **kw: (seen.append(args), orig1(*args, **kw))
         pool.region_update_device(r1, host, ("met0", "met1"))
         assert len(seen) == 2
+
+
+def test_faithful_rng_fused_equals_module_path_with_sorts(rt, golden_chain):
+    """Faithful mode (the reference default, rng.py:105-126): per-device
+    streams seeded rank + 83*device, draws indexed by position in the
+    device's range.  The fused kernel (draws in-kernel, keyed through the
+    id row, box sorts between steps) reproduces the module-by-module path
+    bit for bit on 3 devices."""
+    _, driver, _, ms, _ = rt
+    g = golden_chain
+    mets = [snapshot_from(g, "m0"), snapshot_from(g, "m1")]
+    ctl = _ctl(ms, output_dt=1e9, t_stop=1800.0, rng_mode="faithful", mpi_rank=1)
+    outs = []
+    for fused in (True, False):
+        ens = _ens(ms, g, "init")
+        status, cache = driver.run_simulation(ctl, ens, mets, num_devices=3, fused=fused,
+                                              sort_every=2 if fused else 0)
+        assert status == 0
+        outs.append(np.stack([ens.lon, ens.lat, ens.p, ens.time, *ens.q, *cache.uvwp]))
+    np.testing.assert_array_equal(outs[0], outs[1])
