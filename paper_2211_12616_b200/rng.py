@@ -99,6 +99,9 @@ def generate_random_nums(rng: RngState, step_index: int, work: WorkRange, device
     else:
         seed = rng.seed_global
     ctx.ensure_capacity(work.end, with_batch=True)
+    # key the draws by global index: slots [start, end) hold particles
+    # [start, end) on this scratch context (another call may have left ids)
+    ctx.ids_reset(work.start, n, work.start)
     ctx.rng_fill(_capi.RNG_MODES[rng.mode], seed, step_index, work.start, work.end)
     s = work.slice
     batch.convection[s] = ctx.d2h(_capi.F_RND_CONV, 0, work.start, n)

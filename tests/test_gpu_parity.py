@@ -339,3 +339,21 @@ def test_interpolate_irregular_axes_bit_exact(b200):
     ref = np.stack(orc.sample(orc.Snapshot.like(m0), orc.Snapshot.like(m1), t, lon, lat, p,
                               ("u", "v", "w", "T")))
     exact(got, ref)
+
+
+def test_rng_fill_unaffected_by_earlier_id_layouts(b200):
+    """The scratch context may carry an id row from an earlier call
+    (statistics, sorts); the host-path fill still keys draws by global index."""
+    phys, rng, ms = b200
+    from paper_2211_12616_b200 import output
+    from paper_2211_12616_b200.partition import WorkRange
+    ens = ms.ParticleEnsemble(50, np.zeros(50), np.full(50, 500.0), np.zeros(50),
+                              np.zeros(50), np.zeros(50), np.zeros((6, 50)))
+    output.group_stats(ms.Control(ens_group_slot=5, nq=6), ens, work=WorkRange(0, 10, 40))
+    r = rng.module_rng_init(ms.Control(rng_mode="counter", rng_seed_global=77), 1)
+    b = rng.batch_allocate(1000)
+    rng.generate_random_nums(r, 3, WorkRange(0, 100, 900), 0, b)
+    conv, turb, meso = orc.counter_batch(77, 3, 100, 900)
+    exact(b.convection[100:900], conv)
+    np.testing.assert_allclose(b.diff_turb.reshape(-1, 3)[100:900], turb, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(b.diff_meso.reshape(-1, 3)[100:900], meso, rtol=1e-12, atol=1e-12)
