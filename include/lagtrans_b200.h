@@ -227,6 +227,15 @@ int lt_grid_counts(lt_ctx *ctx, int32_t nx, int32_t ny, int64_t start, int64_t e
 int lt_group_stats(lt_ctx *ctx, int32_t slot, int64_t start, int64_t end, int64_t max_groups,
                    int64_t *ngroups, int64_t *gid, int64_t *count, double *mean, double *std);
 
+/* write_atm (output.py:17-25): one CSV row per particle "time,p,zeta,lon,
+   lat,q0.." with every double formatted exactly as Python's repr() — the
+   reference's bytes — by `threads` host threads (0: all cores).  q is nq
+   rows of q_stride doubles.  lt_format_double formats one value. */
+int lt_write_atm(const char *path, int64_t n, int32_t nq, const double *time, const double *p,
+                 const double *zeta, const double *lon, const double *lat, const double *q,
+                 int64_t q_stride, int32_t threads);
+int lt_format_double(double x, char *out, int32_t cap, int32_t *len);
+
 /* event timing of the last lt_run / lt_sort_by_box on this context */
 int lt_timing(lt_ctx *ctx, int32_t enable);
 int lt_last_elapsed_ms(lt_ctx *ctx, float *ms);

@@ -19,7 +19,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIBDIR = PKG / "_lib"
 LIB = LIBDIR / "liblagtrans_b200.so"
-SOURCES = ["lt_capi.cu", "lt_kernels.cu", "lt_step.cu", "lt_output.cu"]
+SOURCES = ["lt_capi.cu", "lt_kernels.cu", "lt_step.cu", "lt_output.cu", "lt_host.cpp"]
 HEADERS = ["lt_device.cuh", "lt_step.cuh", "lt_kernels.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "--expt-relaxed-constexpr",
@@ -63,7 +63,7 @@ def build(force: bool = False, verbose: bool = False, outdir: Path | None = None
             raise RuntimeError(f"nvcc failed on {src}:\n{r.stderr}")
         objs.append(str(obj))
     tmp = lib.with_suffix(".so.tmp")
-    cmd = [nvcc(), *ARCH, "-shared", "--cudart", "static", "-o", str(tmp), *objs]
+    cmd = [nvcc(), *ARCH, "-shared", "--cudart", "static", "-o", str(tmp), *objs, "-lpthread"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")

@@ -131,6 +131,8 @@ _PROTOS = {
     "lt_interpolate": ([_P, _I64, _P, _P, _P, _P, _P], C.c_int),
     "lt_grid_counts": ([_P, _I32, _I32, _I64, _I64, _P], C.c_int),
     "lt_group_stats": ([_P, _I32, _I64, _I64, _I64, C.POINTER(_I64), _P, _P, _P, _P], C.c_int),
+    "lt_write_atm": ([C.c_char_p, _I64, _I32, _P, _P, _P, _P, _P, _P, _I64, _I32], C.c_int),
+    "lt_format_double": ([_D, C.c_char_p, _I32, C.POINTER(_I32)], C.c_int),
     "lt_run_host": ([_P, C.POINTER(LtControl), _U32, _I64, _I64, _I64, _U64,
                      C.POINTER(LtHostSoa), _I64], C.c_int),
 }

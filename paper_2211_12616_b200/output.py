@@ -127,6 +127,30 @@ def pool_group_stats(ctl, pool):
     return merge_group_stats(parts)
 
 
+def format_double(x: float) -> str:
+    """repr(float(x)) computed by the library (lt_format_double)."""
+    lib = capi.load()
+    buf = C.create_string_buffer(40)
+    n = C.c_int32(0)
+    capi.check(lib.lt_format_double(float(x), buf, 40, C.byref(n)))
+    return buf.value.decode()
+
+
+def write_atm(ens, path, threads: int = 0) -> None:
+    """output.py:17-25, byte for byte, formatted by native threads
+    (lt_write_atm) instead of a per-particle Python loop."""
+    lib = capi.load()
+    n = int(ens.np)
+    rows = [np.ascontiguousarray(getattr(ens, k)[:n], dtype=np.float64)
+            for k in ("time", "p", "zeta", "lon", "lat")]
+    q = np.ascontiguousarray(ens.q[:, :n], dtype=np.float64)
+    nq = q.shape[0]
+    rc = lib.lt_write_atm(str(path).encode(), n, nq, *[capi.ptr(r) for r in rows],
+                          capi.ptr(q) if nq else None, n, int(threads))
+    if rc != capi.LT_OK:
+        raise OSError(f"lt_write_atm failed for {path}")
+
+
 def write_grid(ctl, ens, path) -> None:
     """output.py:28-44 with the counts from the GPU."""
     nx, ny = int(ctl.grid_nx), int(ctl.grid_ny)

@@ -297,10 +297,13 @@ def gen_output():
     with tempfile.TemporaryDirectory() as d:
         output.write_grid(ctl, ens, Path(d) / "grid.csv")
         output.write_ens(ctl, ens, Path(d) / "ens.csv")
+        output.write_atm(ens, Path(d) / "atm.csv")
+        atm_csv = (Path(d) / "atm.csv").read_text()
         grid_csv = (Path(d) / "grid.csv").read_text()
         ens_csv = (Path(d) / "ens.csv").read_text()
     np.savez_compressed(OUT / "output.npz", **ens_arrays("ens", ens), grid_nx=36, grid_ny=18,
-                        slot=5, grid_csv=np.array(grid_csv), ens_csv=np.array(ens_csv))
+                        slot=5, grid_csv=np.array(grid_csv), ens_csv=np.array(ens_csv),
+                        atm_csv=np.array(atm_csv))
 
 
 if __name__ == "__main__":
