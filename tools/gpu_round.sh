@@ -12,7 +12,7 @@ timeout 600 python tools/fast_error.py > $OUT/fast_error.log 2>&1
 if [ -n "$EXTRA_BENCH" ]; then timeout 900 python bench.py $EXTRA_BENCH > $OUT/bench_extra.log 2>&1; fi
 if [ -z "$NO_NCU" ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
-    --log-file $OUT/launches.csv python bench.py --steps 12 --warmup 3 --no-cpu --e2e-steps 0 --alt-steps 0 > $OUT/ncu_launch_run.log 2>&1
+    --log-file $OUT/launches.csv python bench.py --steps 14 --warmup 3 --no-cpu --e2e-steps 0 --alt-steps 0 > $OUT/ncu_launch_run.log 2>&1
   for prec in fast exact; do
     timeout 900 ncu --set full --clock-control none --import-source on -k regex:step_kernel -s 3 -c 1 \
       -f -o $OUT/step_${prec} python bench.py --steps 2 --warmup 3 --no-cpu --e2e-steps 0 --alt-steps 0 \
