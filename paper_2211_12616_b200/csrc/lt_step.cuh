@@ -194,13 +194,30 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
     const bool act = dt > 0.0;
 
     // random draws (rng.py:156-181) are made where they are consumed, which
-    // keeps them out of the registers live across the advection gathers
+    // keeps them out of the registers live across the advection gathers —
+    // except on the fast counter path, below
     const bool want_turb = (mods & M_TURB) && (ctl.turb_dx != 0.0 || ctl.turb_dz != 0.0);
     const bool want_meso = (mods & M_MESO) && ctl.turb_meso != 0.0;
     const bool want_conv = (mods & M_CONVECTION) && ctl.conv_prob != 0.0;
     const uint64_t gid = (RM >= 0 || (a.flags & F_RNG_INKERNEL)) && (want_turb || want_meso || want_conv)
                              ? (a.ids ? static_cast<uint64_t>(a.ids[s]) : static_cast<uint64_t>(s))
                              : 0ull;
+#ifndef LT_LATE_DRAWS
+    // fast counter path: the six normals are pure ALU work on the id, done
+    // before the first gather so they fill issue slots the gathers leave idle
+    float early[6];
+    if (FAST && RM == RNG_COUNTER && act) {
+      double z[3];
+      if (want_turb) {
+        O::normals(ctl.rng_seed_global, a.step, gid, 1, z);
+        early[0] = float(z[0]); early[1] = float(z[1]); early[2] = float(z[2]);
+      }
+      if (want_meso) {
+        O::normals(ctl.rng_seed_global, a.step, gid, 2, z);
+        early[3] = float(z[0]); early[4] = float(z[1]); early[5] = float(z[2]);
+      }
+    }
+#endif
 
     // physics.py:225-235 (module_isosurf_init)
     if ((mods & M_ISOSURF_INIT) && ctl.isosurf_mode != ISO_OFF) {
@@ -239,6 +256,10 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
     // post-hop lon/lat and pre-hop p (numpy view aliasing)
     if (want_turb && act) {
       double xt[3];
+#ifndef LT_LATE_DRAWS
+      if (FAST && RM == RNG_COUNTER) { xt[0] = early[0]; xt[1] = early[1]; xt[2] = early[2]; }
+      else
+#endif
       draws<O, RM>(a, s, gid, 1, xt);
       if (ctl.turb_dx > 0.0) {
         const double sig = sqrt(2.0 * ctl.turb_dx * dt);
@@ -265,6 +286,10 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
       for (int f = 0; f < 3; ++f) up[f] = ld_state(a.uvwp[f] + s);
 #endif
       double xm[3];
+#ifndef LT_LATE_DRAWS
+      if (FAST && RM == RNG_COUNTER) { xm[0] = early[3]; xm[1] = early[4]; xm[2] = early[5]; }
+      else
+#endif
       draws<O, RM>(a, s, gid, 2, xm);
       Corners<Rec> q;
       gather(a.met.s0, a.met, O::cell(a.met, lon, lat, p), q);
