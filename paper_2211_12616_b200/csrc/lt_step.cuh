@@ -205,16 +205,19 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
 #ifndef LT_LATE_DRAWS
     // fast counter path: the six normals are pure ALU work on the id, done
     // before the first gather so they fill issue slots the gathers leave idle
+    // (the exact path measured slower this way: its fp64 normals cost twice
+    // the registers)
+    constexpr bool kEarly = FAST && RM == RNG_COUNTER;
     float early[6];
-    if (FAST && RM == RNG_COUNTER && act) {
+    if (kEarly && act) {
       double z[3];
       if (want_turb) {
         O::normals(ctl.rng_seed_global, a.step, gid, 1, z);
-        early[0] = float(z[0]); early[1] = float(z[1]); early[2] = float(z[2]);
+        early[0] = z[0]; early[1] = z[1]; early[2] = z[2];
       }
       if (want_meso) {
         O::normals(ctl.rng_seed_global, a.step, gid, 2, z);
-        early[3] = float(z[0]); early[4] = float(z[1]); early[5] = float(z[2]);
+        early[3] = z[0]; early[4] = z[1]; early[5] = z[2];
       }
     }
 #endif
@@ -257,7 +260,7 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
     if (want_turb && act) {
       double xt[3];
 #ifndef LT_LATE_DRAWS
-      if (FAST && RM == RNG_COUNTER) { xt[0] = early[0]; xt[1] = early[1]; xt[2] = early[2]; }
+      if (kEarly) { xt[0] = early[0]; xt[1] = early[1]; xt[2] = early[2]; }
       else
 #endif
       draws<O, RM>(a, s, gid, 1, xt);
@@ -287,7 +290,7 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
 #endif
       double xm[3];
 #ifndef LT_LATE_DRAWS
-      if (FAST && RM == RNG_COUNTER) { xm[0] = early[3]; xm[1] = early[4]; xm[2] = early[5]; }
+      if (kEarly) { xm[0] = early[3]; xm[1] = early[4]; xm[2] = early[5]; }
       else
 #endif
       draws<O, RM>(a, s, gid, 2, xm);
