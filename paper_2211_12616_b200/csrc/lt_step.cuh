@@ -56,10 +56,6 @@ __device__ __forceinline__ double ld_state(const double* p) { return *p; }
 __device__ __forceinline__ void st_state(double* p, double v) { *p = v; }
 #endif
 
-__device__ __forceinline__ void prefetch_l1(const void* ptr) {
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(ptr));
-}
-
 #ifndef LT_STEP_BLOCK
 #define LT_STEP_BLOCK 256
 #endif
@@ -174,11 +170,6 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
       if (a.ids && (mods & (M_TURB | M_MESO | M_CONVECTION))) prefetch_l2(a.ids + nx);
     }
 #endif
-#ifdef LT_PF_L1_UVWP
-    if (mods & M_MESO) {
-      prefetch_l1(a.uvwp[0] + s); prefetch_l1(a.uvwp[1] + s); prefetch_l1(a.uvwp[2] + s);
-    }
-#endif
     double time = ld_state(a.time + s), lon = ld_state(a.lon + s), lat = ld_state(a.lat + s),
            p = ld_state(a.p + s);
 
@@ -281,13 +272,6 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
 
     // physics.py:150-188 (module_diffusion_meso): AR(1) with met0 cell spread
     if (want_meso && act) {
-#ifdef LT_MESO_EARLY
-      // issue the AR(1) state loads before the draws and the gather so
-      // their latency overlaps that work
-      double up[3];
-#pragma unroll
-      for (int f = 0; f < 3; ++f) up[f] = ld_state(a.uvwp[f] + s);
-#endif
       double xm[3];
 #ifndef LT_LATE_DRAWS
       if (kEarly) { xm[0] = early[3]; xm[1] = early[4]; xm[2] = early[5]; }
@@ -303,11 +287,7 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
 #pragma unroll
       for (int f = 0; f < 3; ++f) {
         const double sigma = ctl.turb_meso * O::spread(q, f);
-#ifdef LT_MESO_EARLY
-        pert[f] = r * up[f] + amp * sigma * xm[f];
-#else
         pert[f] = r * ld_state(a.uvwp[f] + s) + amp * sigma * xm[f];
-#endif
         st_state(a.uvwp[f] + s, pert[f]);
       }
       const double nlon = lon + O::over_cos(pert[0] * dt * kDegPerM, lat);
