@@ -114,8 +114,8 @@ class Engine:
     def bind_met(self, met0, met1) -> None:
         """Load the first snapshot pair into slots 0 and 1."""
         self.ctx.set_grid(met0.lons, met0.lats, met0.levs)
-        self.ctx.load_met(0, met0)
-        self.ctx.load_met(1, met1)
+        self.ctx.load_met(0, met0, key=met_fingerprint(met0))
+        self.ctx.load_met(1, met1, key=met_fingerprint(met1))
         self._met_slots = (0, 1)
         self._staged = None
         self.ctx.use_met(0, 1)
