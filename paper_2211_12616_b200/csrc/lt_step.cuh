@@ -69,12 +69,17 @@ template <class Rec, bool FAST>
 struct Ops {
   static constexpr bool kFast = false;
   __device__ static void sample(const MetView<Rec>& m, double t, double lon, double lat,
-                                double p, int fmask, double out[4]) {
-    lt::sample(m, t, lon, lat, p, fmask, out);
+                                double p, int fmask, double out[4], uint32_t* col = nullptr) {
+    lt::sample(m, t, lon, lat, p, fmask, out, col);
   }
   __device__ static double over_cos(double x, double lat) { return x / cos_lat(lat); }
   __device__ static uint32_t cell(const MetView<Rec>& m, double lon, double lat, double p) {
     return cell_of(m, lon, lat, p).r00;
+  }
+  // the cell of a point whose lon/lat column is already known
+  __device__ static uint32_t cell_in_column(const MetView<Rec>& m, uint32_t col, double p) {
+    double frev;
+    return col * (m.nz - 1) + (m.nz - 2 - locate(m.lev, p, frev));
   }
   template <class T>
   __device__ static double spread(const CornersT<T>& q, int f) { return corner_std(q, f); }
@@ -87,12 +92,16 @@ template <>
 struct Ops<RecF, true> {
   static constexpr bool kFast = true;
   __device__ static void sample(const MetView<RecF>& m, double t, double lon, double lat,
-                                double p, int fmask, double out[4]) {
-    sample_fast(m, t, lon, lat, p, fmask, out);
+                                double p, int fmask, double out[4], uint32_t* col = nullptr) {
+    sample_fast(m, t, lon, lat, p, fmask, out, col);
   }
   __device__ static double over_cos(double x, double lat) { return x * inv_cos_lat_fast(lat); }
   __device__ static uint32_t cell(const MetView<RecF>& m, double lon, double lat, double p) {
     return cell_fast(m, lon, lat, p).r00;
+  }
+  __device__ static uint32_t cell_in_column(const MetView<RecF>& m, uint32_t col, double p) {
+    float frev;
+    return col * (m.nz - 1) + (m.nz - 2 - locate_fast(m.lev, p, frev));
   }
   __device__ static double spread(const CornersT<float>& q, int f) { return corner_std_f(q, f); }
   __device__ static void normals(uint64_t seed, int64_t step, uint64_t gid, int stream, double z[3]) {
@@ -246,6 +255,9 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
       time = time + dt;
     }
 
+    constexpr uint32_t kNoColumn = 0xFFFFFFFFu;
+    uint32_t tcol = kNoColumn;  // lon/lat column of the turb T sample (reused by meso)
+
     // physics.py:119-147 (module_diffusion_turb); the vertical part sees the
     // post-hop lon/lat and pre-hop p (numpy view aliasing)
     if (want_turb && act) {
@@ -263,7 +275,7 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
       }
       if (ctl.turb_dz > 0.0) {
         double v[4];
-        O::sample(a.met, time, lon, lat, p, 8, v);
+        O::sample(a.met, time, lon, lat, p, 8, v, &tcol);
         const double dz = sqrt(2.0 * ctl.turb_dz * dt) * xt[2];
         const double rho = 100.0 * p / (kRAir * v[3]);
         p = p + (-(rho * kG0 * dz) / 100.0);
@@ -279,7 +291,10 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
 #endif
       draws<O, RM>(a, s, gid, 2, xm);
       Corners<Rec> q;
-      gather(a.met.s0, a.met, O::cell(a.met, lon, lat, p), q);
+      // the vertical hop moved only p: the T sample's lon/lat column holds
+      const uint32_t r00 = tcol != kNoColumn ? O::cell_in_column(a.met, tcol, p)
+                                             : O::cell(a.met, lon, lat, p);
+      gather(a.met.s0, a.met, r00, q);
       double r = 1.0 - 2.0 * dt / ctl.met_dt;
       r = fmin(fmax(r, 0.0), 1.0);
       const double amp = sqrt(1.0 - r * r);
