@@ -20,6 +20,23 @@ sys.path.insert(0, str(ROOT))
 from oracle import lagtrans_oracle as orc  # noqa: E402
 
 
+def _ensure_library():
+    """Build liblagtrans_b200.so in-tree when a fresh checkout lacks it (it
+    is git-ignored); nvcc cross-compiles for sm_100a without a GPU."""
+    lib = ROOT / "paper_2211_12616_b200" / "_lib" / "liblagtrans_b200.so"
+    if lib.exists():
+        return
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "_lt_build", ROOT / "paper_2211_12616_b200" / "_build.py")
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    mod.build()
+
+
+_ensure_library()
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200)")
     config.addinivalue_line("markers", "slow: long-running")
