@@ -506,11 +506,18 @@ def main():
                        "step / D2H on three streams, every step (wall clock, max over ranks)"}
 
     traffic = None
+    issue = None
     prof = ROOT / "profiles" / f"ncu_step_{wl}.json"
     if prof.exists():
         pj = json.loads(prof.read_text()).get(args.precision, {})
         if pj.get("dram_bytes_per_particle_step") is not None:
             traffic = pj["dram_bytes_per_particle_step"] * work.size
+        if pj.get("issue_active_pct") is not None:
+            # the bound that binds: instruction issue / latency, from the same capture
+            issue = {"issue_active": pj["issue_active_pct"] / 100.0,
+                     "thread_instructions_per_particle_step":
+                         pj.get("thread_instructions_per_particle"),
+                     "source": f"profiles/ncu_step_{wl}.json (ncu --set full)"}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
@@ -549,7 +556,7 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "step_kernel", "kernel_ms": kern_avg,
-                         "algorithmic_bytes_per_particle_step": b,
+                         "algorithmic_bytes_per_particle_step": b, "issue": issue,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks
                          else "fallback"},
             "alt_precision": other,
