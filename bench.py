@@ -27,8 +27,14 @@ reference` time the CPU oracle (a numpy restatement of the reference,
 oracle/) on the host's cores on a bounded particle sample of the same
 workload.  `precision` "fast" (default) computes interpolation weights and
 sums and the Box-Muller transform in fp32 with fp64 particle state; it stays
-within the north star's 1e-5 run tolerance (tests/test_gpu_engine.py); the
-line also carries the bit-faithful "exact" kernel's numbers.
+within the north star's 1e-5 run tolerance (tests/test_gpu_engine.py).
+`--rng philox` (default) is the north star's counter-based generator keyed
+by the full 32-bit particle id — the reference's splitmix64 counter key
+packs only 24 bits of index, so at 1e8 particles it would hand particles i
+and i + 2^24 identical draws; `counter` reproduces the reference's words
+bit for bit.  The line also carries the same measurement with the
+bit-faithful "exact" kernels (`alt_precision`) and with the counter words
+(`alt_rng`).
 """
 
 from __future__ import annotations
@@ -149,12 +155,12 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def make_ctl(wl, precision="fast"):
+def make_ctl(wl, precision="fast", rng_mode="counter"):
     from paper_2211_12616_b200.model_state import Control
     cfg = WORKLOADS[wl]
     kw = dict(np_max=10 ** 10, t_stop=30 * 86400.0, dt_model=180.0,
               met_dt=cfg.get("met_dt", 10800.0), turb_dx=50.0, turb_dz=0.1, turb_meso=0.16,
-              rng_mode="counter", rng_seed_global=12616, precision=precision)
+              rng_mode=rng_mode, rng_seed_global=12616, precision=precision)
     kw.update(cfg.get("ctl", {}))
     return Control(**kw)
 
@@ -335,6 +341,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--precision", default="fast", choices=("exact", "fast"))
     ap.add_argument("--met-store", default="f32", choices=("f32", "f64"))
+    ap.add_argument("--rng", default="philox", choices=("counter", "faithful", "philox"))
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     wl = args.workload
@@ -362,7 +369,7 @@ def main():
     n_tot = cfg["n"]
     mask = engine.modules_mask(cfg["chain"])
     work = sharding.shard_range(n_tot, ws, rank)
-    ctl = make_ctl(wl, args.precision)
+    ctl = make_ctl(wl, args.precision, args.rng)
 
     mets = build_met(wl, rank, ws)
     eng = engine.Engine(device=gpu, first_id=work.start, met_precision=args.met_store,
@@ -451,16 +458,21 @@ def main():
     peak = peaks.get("hbm_gbs", 6650.0)
     achieved = b * work.size / (kern_avg / 1e3) / 1e9
 
-    # the other precision's kernels on the same state, same protocol
-    other = None
+    # the same steps with the other kernels, same state, same protocol:
+    # the other precision, and the reference's bit-identical counter words
+    def alt_run(precision, rng, k):
+        t2, k2, clk2, _, _ = timed(make_ctl(wl, precision, rng), k)
+        return {"precision": precision, "rng": rng, "value": n_tot * k / (t2 / 1e3),
+                "ms_per_step": t2 / k, "kernel_ms": k2,
+                "roofline_frac": b * work.size / (k2 / 1e3) / 1e9 / peak, "steps": k,
+                "clocks": clk2}
+
+    other = alt_rng = None
     k_other = args.steps if args.alt_steps < 0 else args.alt_steps
     if k_other > 0:
-        alt = "exact" if args.precision == "fast" else "fast"
-        t2, k2, clk2, _, _ = timed(make_ctl(wl, alt), k_other)
-        other = {"precision": alt, "value": n_tot * k_other / (t2 / 1e3),
-                 "ms_per_step": t2 / k_other, "kernel_ms": k2,
-                 "roofline_frac": b * work.size / (k2 / 1e3) / 1e9 / peak, "steps": k_other,
-                 "clocks": clk2}
+        other = alt_run("exact" if args.precision == "fast" else "fast", args.rng, k_other)
+        if args.rng != "counter":
+            alt_rng = alt_run(args.precision, "counter", k_other)
 
     # e2e: the public host-buffer API (Engine.step_host -> lt_run_host): the
     # shard's SoA sits in pinned host memory; every step streams it through
@@ -548,7 +560,10 @@ def main():
                        "modules": list(cfg["chain"]),
                        "met_store": f"{args.met_store} node-pair records", "state": "fp64 SoA",
                        "precision": args.precision,
-                       "rng": "counter (reference splitmix64 words), in-kernel",
+                       "rng": f"{args.rng} (reference splitmix64 words), in-kernel"
+                              if args.rng != "philox" else
+                              "philox4x32-10 keyed by (seed, step, 32-bit particle id), "
+                              "in-kernel (the north star's counter-based generator)",
                        "sort_every": sort_every, "met_rotations_timed": rots,
                        "parallelism": f"particles sharded x{ws}, met replicated (NCCL broadcast)",
                        "l2": "inputs larger than L2 (state %.1f GB/GPU, met %.1f GB)" % (
@@ -559,7 +574,7 @@ def main():
                          "algorithmic_bytes_per_particle_step": b, "issue": issue,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks
                          else "fallback"},
-            "alt_precision": other,
+            "alt_precision": other, "alt_rng": alt_rng,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": launches,
         }), flush=True)

@@ -38,6 +38,7 @@ static cudaError_t launch_prec(const StepArgs<Rec>& a, cudaStream_t st) {
   if (a.modules == kChainAdvDiff && (a.flags & F_RNG_INKERNEL)) {
     if (a.ctl.rng_mode == RNG_COUNTER) return launch_fixed<Rec, kChainAdvDiff, FAST, RNG_COUNTER>(a, st);
     if (a.ctl.rng_mode == RNG_PHILOX) return launch_fixed<Rec, kChainAdvDiff, FAST, RNG_PHILOX>(a, st);
+    if (a.ctl.rng_mode == RNG_FAITHFUL) return launch_fixed<Rec, kChainAdvDiff, FAST, RNG_FAITHFUL>(a, st);
   }
   if (a.modules == kChainAdvDiff) return launch_fixed<Rec, kChainAdvDiff, FAST, -1>(a, st);
   if (a.modules == kChainAdv) return launch_fixed<Rec, kChainAdv, FAST, -1>(a, st);

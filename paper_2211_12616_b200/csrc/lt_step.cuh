@@ -111,8 +111,8 @@ struct Ops<RecF, true> {
 
 // Draws of one stream for particle slot s / global id gid: stream 0 = the
 // convection uniform (x[0]), 1 = turbulent normals, 2 = mesoscale normals.
-// RM >= 0 fixes the in-kernel generator at compile time (RNG_COUNTER or
-// RNG_PHILOX, no batch); RM = -1 decides at run time.
+// RM >= 0 fixes the in-kernel generator at compile time (RNG_COUNTER,
+// RNG_PHILOX or RNG_FAITHFUL, no batch); RM = -1 decides at run time.
 template <class O, int RM, class Rec>
 __device__ __forceinline__ void draws(const StepArgs<Rec>& a, int64_t s, uint64_t gid, int stream,
                                       double x[3]) {
@@ -124,6 +124,10 @@ __device__ __forceinline__ void draws(const StepArgs<Rec>& a, int64_t s, uint64_
   }
   if (RM == RNG_PHILOX) {
     philox_stream(ctl.rng_seed_global, a.step, gid, stream, x);
+    return;
+  }
+  if (RM == RNG_FAITHFUL) {
+    faithful_stream(a.faithful_state, gid - static_cast<uint64_t>(a.faithful_base), stream, x);
     return;
   }
   if (!(a.flags & F_RNG_INKERNEL)) {  // the caller's RandomBatch
@@ -203,21 +207,28 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
                              ? (a.ids ? static_cast<uint64_t>(a.ids[s]) : static_cast<uint64_t>(s))
                              : 0ull;
 #ifndef LT_LATE_DRAWS
-    // fast counter path: the six normals are pure ALU work on the id, done
-    // before the first gather so they fill issue slots the gathers leave idle
+    // fast path with a compile-time generator: the six normals are pure ALU
+    // work on the id, done (fp32, SFU) before the first gather so they fill
+    // issue slots the gathers leave idle
     // (the exact path measured slower this way: its fp64 normals cost twice
     // the registers)
-    constexpr bool kEarly = FAST && RM == RNG_COUNTER;
+    constexpr bool kEarly = FAST && RM >= 0;
     float early[6];
     if (kEarly && act) {
-      double z[3];
-      if (want_turb) {
-        O::normals(ctl.rng_seed_global, a.step, gid, 1, z);
-        early[0] = z[0]; early[1] = z[1]; early[2] = z[2];
-      }
-      if (want_meso) {
-        O::normals(ctl.rng_seed_global, a.step, gid, 2, z);
-        early[3] = z[0]; early[4] = z[1]; early[5] = z[2];
+      if (RM == RNG_FAITHFUL) {
+        faithful_normals_fast(a.faithful_state, gid - static_cast<uint64_t>(a.faithful_base), early);
+      } else if (RM == RNG_PHILOX) {
+        philox_normals_fast(ctl.rng_seed_global, a.step, gid, early);
+      } else {
+        double z[3];
+        if (want_turb) {
+          O::normals(ctl.rng_seed_global, a.step, gid, 1, z);
+          early[0] = z[0]; early[1] = z[1]; early[2] = z[2];
+        }
+        if (want_meso) {
+          O::normals(ctl.rng_seed_global, a.step, gid, 2, z);
+          early[3] = z[0]; early[4] = z[1]; early[5] = z[2];
+        }
       }
     }
 #endif

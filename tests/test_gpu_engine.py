@@ -302,3 +302,48 @@ def test_group_stats_with_home_order_q(eng):
     np.testing.assert_array_equal(after[1], oc)
     np.testing.assert_allclose(after[2], om, rtol=1e-12)
     np.testing.assert_array_equal(before[1], after[1])
+
+
+def test_faithful_mode_production_chain(eng):
+    """The adv+turb+meso chain with the reference's default faithful RNG
+    (compile-time generator): exact kernels against the oracle stepping
+    with the same per-device stream; fast kernels within tolerance."""
+    engine, ms, syn = eng
+    m0, m1 = syn.analytic_pair(dlon=5.0, dlat=5.0, nlev=30, t0=0.0, t1=10800.0)
+    ens = syn.particles(20000, seed=13)
+    kw = dict(t_stop=86400.0, dt_model=180.0, met_dt=10800.0, rng_mode="faithful", mpi_rank=3)
+    st = {"time": ens.time.copy(), "lon": ens.lon.copy(), "lat": ens.lat.copy(),
+          "p": ens.p.copy(), "uvwp": np.zeros((3, ens.np)), "iso_var": np.zeros(ens.np),
+          "q": np.zeros((5, ens.np))}
+    s0, s1 = orc.Snapshot.like(m0), orc.Snapshot.like(m1)
+    state = orc.seed_for(3, 0)
+    for step in range(12):
+        state = orc.full_step(ms.Control(**kw), s0, s1, st, 0, ens.np, step, rng_state=state,
+                              modules=("advection", "turb", "meso", "position"))
+    exact = _engine_run(engine, m0, m1, ens, ms.Control(**kw), 12, engine.ADV_DIFF, 5)
+    for k in ("lon", "lat", "p", "time"):
+        np.testing.assert_allclose(getattr(exact, k), st[k], rtol=1e-10, atol=1e-9)
+    fast = _engine_run(engine, m0, m1, ens, ms.Control(precision="fast", **kw), 12,
+                       engine.ADV_DIFF, 5)
+    assert np.abs((fast.lon - exact.lon + 180.0) % 360.0 - 180.0).max() / 360.0 <= 1e-6
+    assert (np.abs(fast.p - exact.p) / exact.p).max() <= 1e-6
+
+
+@pytest.mark.parametrize("precision", ["exact", "fast"])
+def test_philox_production_chain_brownian_variance(eng, precision):
+    """Philox (the north star's counter-based generator, full 32-bit ids):
+    Brownian variance 2 K t within 5 % (acceptance c5) through the fused
+    production chain, both precisions."""
+    engine, ms, syn = eng
+    lons, lats, levs = syn.grid(30.0, 10.0, 7)
+    shape = (lons.size, lats.size, levs.size)
+    z = np.zeros(shape)
+    met = ms.met_periodic(ms.MeteoField(0.0, lons, lats, levs, z, z, z, np.full(shape, 250.0)))
+    n = 200_000
+    ens = syn.particles(n, seed=2, lat_span=0.0)
+    ens.lon[:] = 0.0
+    ctl = ms.Control(t_stop=1e6, dt_model=1000.0, met_dt=10800.0, turb_dx=50.0, turb_dz=0.0,
+                     turb_meso=0.0, rng_mode="philox", rng_seed_global=11, precision=precision)
+    out = _engine_run(engine, met, met, ens, ctl, 10, engine.ADV_DIFF)
+    var = np.var(out.lon / (180.0 / (np.pi * 6371000.0)))
+    assert var == pytest.approx(2.0 * 50.0 * 1e4, rel=0.05)
