@@ -347,3 +347,20 @@ def test_philox_production_chain_brownian_variance(eng, precision):
     out = _engine_run(engine, met, met, ens, ctl, 10, engine.ADV_DIFF)
     var = np.var(out.lon / (180.0 / (np.pi * 6371000.0)))
     assert var == pytest.approx(2.0 * 50.0 * 1e4, rel=0.05)
+
+
+def test_fast_precision_philox_within_tolerance(eng):
+    """The headline configuration (fast kernels, Philox) against the exact
+    kernels on the same draws: a 24 h cfg2-style run stays inside 1e-5."""
+    engine, ms, syn = eng
+    m0, m1 = syn.analytic_pair(1.0, 1.0, 60, 0.0, 10800.0)
+    ens = syn.particles(100_000, seed=22)
+    kw = dict(t_stop=86400.0, dt_model=180.0, met_dt=10800.0, rng_mode="philox",
+              rng_seed_global=5)
+    exact = _engine_run(engine, m0, m1, ens, ms.Control(**kw), 480, engine.ADV_DIFF, 15)
+    fast = _engine_run(engine, m0, m1, ens, ms.Control(precision="fast", **kw), 480,
+                       engine.ADV_DIFF, 15)
+    dlon = np.abs((fast.lon - exact.lon + 180.0) % 360.0 - 180.0)
+    assert dlon.max() / 360.0 <= 1e-5
+    assert np.abs(fast.lat - exact.lat).max() / 180.0 <= 1e-5
+    assert (np.abs(fast.p - exact.p) / exact.p).max() <= 1e-5

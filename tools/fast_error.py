@@ -25,7 +25,9 @@ def run(ctl, m0, m1, ens, steps, sort_every=40):
 
 m0, m1 = synthetic.analytic_pair(1.0, 1.0, 60, 0.0, 10800.0)
 ens = synthetic.particles(200_000, seed=21)
-kw = dict(t_stop=86400.0, dt_model=180.0, met_dt=10800.0, rng_mode="counter", rng_seed_global=5)
+mode = sys.argv[1] if len(sys.argv) > 1 else "counter"
+kw = dict(t_stop=86400.0, dt_model=180.0, met_dt=10800.0, rng_mode=mode, rng_seed_global=5)
+print("rng", mode)
 ex = run(ms.Control(**kw), m0, m1, ens, 480)
 fa = run(ms.Control(precision="fast", **kw), m0, m1, ens, 480)
 rp = np.abs(fa.p - ex.p) / ex.p

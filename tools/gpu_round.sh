@@ -8,7 +8,7 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > 
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > $OUT/smoke.log 2>&1
 timeout 900 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.log 2>&1
 timeout 900 python bench.py ${BENCH_ARGS} > $OUT/bench.log 2>&1
-timeout 600 python tools/fast_error.py > $OUT/fast_error.log 2>&1
+for r in counter philox; do timeout 600 python tools/fast_error.py $r >> $OUT/fast_error.log 2>&1; done
 if [ -n "$EXTRA_BENCH" ]; then timeout 900 python bench.py $EXTRA_BENCH > $OUT/bench_extra.log 2>&1; fi
 if [ -z "$NO_NCU" ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
