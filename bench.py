@@ -500,10 +500,11 @@ def main():
         eng.step_host(ctl, hens, hcache, step, mask, chunk=args.e2e_chunk)   # warm-up
         step += 1
         barrier()
+        # K steps in one call: every step still moves every particle host ->
+        # device -> host; chunks of step s+1 start as chunks of step s land
         t0 = time.perf_counter()
-        for k in range(args.e2e_steps):
-            eng.step_host(ctl, hens, hcache, step, mask, chunk=args.e2e_chunk)
-            step += 1
+        eng.step_host(ctl, hens, hcache, step, mask, chunk=args.e2e_chunk, steps=args.e2e_steps)
+        step += args.e2e_steps
         barrier()
         te = sharding.max_over_ranks([time.perf_counter() - t0], dist, "cuda")[0]
         chain = cfg["chain"]
@@ -514,8 +515,9 @@ def main():
         e2e = {"value": n_tot * args.e2e_steps / te, "unit": "particle-steps/s",
                "h2d_bytes_per_step": 8 * rows_in * n_tot, "d2h_bytes_per_step": 8 * rows_out * n_tot,
                "steps": args.e2e_steps,
-               "path": "Engine.step_host -> lt_run_host: pinned host SoA, chunked H2D / fused "
-                       "step / D2H on three streams, every step (wall clock, max over ranks)"}
+               "path": "Engine.step_host(steps=K) -> lt_run_host_steps: pinned host SoA, every "
+                       "step chunked H2D / fused step / D2H on three streams, pipelined across "
+                       "steps (wall clock, max over ranks)"}
 
     traffic = None
     issue = None

@@ -181,6 +181,13 @@ typedef struct lt_host_soa {
 int lt_run_host(lt_ctx *ctx, const lt_control *ctl, uint32_t modules, int64_t n,
                 int64_t step, int64_t first_id, uint64_t faithful_state,
                 const lt_host_soa *io, int64_t chunk);
+/* nsteps consecutive host-buffer steps (step, step+1, ...; the faithful
+   state advances 7n draws per step): every step still moves every particle
+   host -> device -> host, but chunk c of step s+1 starts as soon as chunk c
+   of step s has landed, so the pipeline fills and drains once per call */
+int lt_run_host_steps(lt_ctx *ctx, const lt_control *ctl, uint32_t modules, int64_t n,
+                      int64_t step, int32_t nsteps, int64_t first_id, uint64_t faithful_state,
+                      const lt_host_soa *io, int64_t chunk);
 
 /* fill the device RandomBatch for [start, end) (rng.py:156-181); counter and
    philox draws are keyed by the slot's global particle id (LT_F_ID) once the

@@ -135,6 +135,8 @@ _PROTOS = {
     "lt_format_double": ([_D, C.c_char_p, _I32, C.POINTER(_I32)], C.c_int),
     "lt_run_host": ([_P, C.POINTER(LtControl), _U32, _I64, _I64, _I64, _U64,
                      C.POINTER(LtHostSoa), _I64], C.c_int),
+    "lt_run_host_steps": ([_P, C.POINTER(LtControl), _U32, _I64, _I64, _I32, _I64, _U64,
+                           C.POINTER(LtHostSoa), _I64], C.c_int),
 }
 EXPORTED = tuple(_PROTOS)
 

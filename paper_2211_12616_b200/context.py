@@ -245,8 +245,9 @@ class DeviceContext:
 
     def run_host(self, ctl, modules: int, n: int, step: int, first_id: int, time, p, lon, lat,
                  uvwp=None, iso_var=None, q=None, faithful_state: int = 0,
-                 chunk: int = 0) -> None:
-        """lt_run_host on C-contiguous float64 host arrays (updated in place)."""
+                 chunk: int = 0, steps: int = 1) -> None:
+        """lt_run_host_steps on C-contiguous float64 host arrays (updated in
+        place): `steps` consecutive steps, each a full host round trip."""
         c = ctl if isinstance(ctl, capi.LtControl) else capi.control_struct(ctl)
         arrs = [time, p, lon, lat]
         for a in arrs + [x for x in (uvwp, iso_var, q) if x is not None]:
@@ -261,9 +262,9 @@ class DeviceContext:
                             capi.ptr(iso_var) if iso_var is not None else None,
                             capi.ptr(q) if q is not None else None, stride,
                             q.shape[0] if q is not None else 0)
-        capi.check(self.lib.lt_run_host(self.h, C.byref(c), modules, n, step, first_id,
-                                        faithful_state & 0xFFFFFFFFFFFFFFFF, C.byref(io),
-                                        chunk))
+        capi.check(self.lib.lt_run_host_steps(self.h, C.byref(c), modules, n, step, int(steps),
+                                              first_id, faithful_state & 0xFFFFFFFFFFFFFFFF,
+                                              C.byref(io), chunk))
 
     def rng_fill(self, mode: int, seed: int, step: int, start: int, end: int) -> None:
         capi.check(self.lib.lt_rng_fill(self.h, mode, seed & 0xFFFFFFFFFFFFFFFF, step, start, end))

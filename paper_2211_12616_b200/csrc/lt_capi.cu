@@ -64,6 +64,7 @@ struct lt_ctx {
   cudaStream_t copy = nullptr;    // met streaming, host-path H2D
   cudaStream_t d2h = nullptr;     // host-path D2H
   std::vector<cudaEvent_t> ring_ev;  // host-path chunk events (3 per ring slot)
+  std::vector<cudaEvent_t> host_ev;  // host-path: chunk k's results are back in host memory
   cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
   cudaEvent_t compute_mark = nullptr;  // last compute-stream work touching met slots
   bool marked = false;
@@ -348,6 +349,7 @@ int lt_ctx_destroy(lt_ctx* c) {
   cudaStreamDestroy(c->copy);
   cudaStreamDestroy(c->d2h);
   for (cudaEvent_t e : c->ring_ev) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->host_ev) cudaEventDestroy(e);
   delete c;
   if (e1 != cudaSuccess || e2 != cudaSuccess)
     return fail(LT_ERR_CUDA, "pending work failed before destroy: %s",
@@ -784,11 +786,22 @@ int lt_run(lt_ctx* c, const lt_control* ctl, uint32_t modules, int64_t start, in
 // refilled before its results have been copied out.
 int lt_run_host(lt_ctx* c, const lt_control* ctl, uint32_t modules, int64_t n, int64_t step,
                 int64_t first_id, uint64_t fstate, const lt_host_soa* io, int64_t chunk) {
+  return lt_run_host_steps(c, ctl, modules, n, step, 1, first_id, fstate, io, chunk);
+}
+
+// nsteps steps, each a full round trip of every particle through the GPU.
+// Particles are independent, so chunk c of step s+1 only has to wait for
+// chunk c of step s to land back in host memory: the pipeline never drains
+// between steps (one fill and one drain per call instead of per step).
+int lt_run_host_steps(lt_ctx* c, const lt_control* ctl, uint32_t modules, int64_t n, int64_t step,
+                      int32_t nsteps, int64_t first_id, uint64_t fstate, const lt_host_soa* io,
+                      int64_t chunk) {
   int rc = check_ctx(c);
   if (rc || (rc = check_particles(c))) return rc;
   if (!io || !io->time || !io->p || !io->lon || !io->lat)
     return fail(LT_ERR_ARG, "host SoA needs time, p, lon and lat");
   if (n < 0) return fail(LT_ERR_ARG, "negative particle count");
+  if (nsteps < 0) return fail(LT_ERR_ARG, "negative step count");
   if (first_id < 0 || first_id + n > (int64_t(1) << 32))
     return fail(LT_ERR_ARG, "particle ids must fit in 32 bits");
   const bool meso = modules & M_MESO;
@@ -802,7 +815,7 @@ int lt_run_host(lt_ctx* c, const lt_control* ctl, uint32_t modules, int64_t n, i
   if (meteo && (io->nq < 5 || c->nq < 5)) return fail(LT_ERR_ARG, "meteo needs 5 q rows");
   if (decay && (ctl->decay_slot >= io->nq || ctl->decay_slot >= c->nq))
     return fail(LT_ERR_ARG, "decay_slot outside the q rows");
-  if (n == 0) return LT_OK;
+  if (n == 0 || nsteps == 0) return LT_OK;
   // the store is scratch for this call: every row in slot order
   c->home_mask = 0;
   c->home_n = 0;
@@ -840,31 +853,44 @@ int lt_run_host(lt_ctx* c, const lt_control* ctl, uint32_t modules, int64_t n, i
   // the copy stream must not overwrite slots the compute stream still reads
   CK(cudaEventRecord(c->compute_mark, c->stream));
   CK(cudaStreamWaitEvent(c->copy, c->compute_mark, 0));
-  for (int64_t k = 0; k < nchunks; ++k) {
-    const int b = static_cast<int>(k % nbuf);
-    const int64_t off = b * chunk, lo = k * chunk, cnt = std::min(chunk, n - lo);
-    cudaEvent_t h2d_done = c->ring_ev[3 * b], run_done = c->ring_ev[3 * b + 1],
-                d2h_done = c->ring_ev[3 * b + 2];
-    if (k >= nbuf) CK(cudaStreamWaitEvent(c->copy, d2h_done, 0));
-    for (const Row& r : rows)
-      if (r.in) CK(cudaMemcpyAsync(r.dev + off, r.host + lo, sizeof(double) * cnt, cudaMemcpyHostToDevice, c->copy));
-    CK(cudaEventRecord(h2d_done, c->copy));
-    CK(cudaStreamWaitEvent(c->stream, h2d_done, 0));
-    CK(launch_iota(c->ids, off, cnt, first_id + lo, c->stream));
-    rc = c->prec == LT_MET_F64
-             ? run_typed<RecD>(c, ctl, modules, off, off + cnt, step, fstate, first_id, LT_RUN_RNG_INKERNEL)
-             : run_typed<RecF>(c, ctl, modules, off, off + cnt, step, fstate, first_id, LT_RUN_RNG_INKERNEL);
-    if (rc) return rc;
-    CK(cudaEventRecord(run_done, c->stream));
-    CK(cudaStreamWaitEvent(c->d2h, run_done, 0));
-    for (const Row& r : rows)
-      if (r.out) CK(cudaMemcpyAsync(r.host + lo, r.dev + off, sizeof(double) * cnt, cudaMemcpyDeviceToHost, c->d2h));
-    CK(cudaEventRecord(d2h_done, c->d2h));
+  while (c->host_ev.size() < static_cast<size_t>(nchunks)) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->host_ev.push_back(e);
   }
+  for (int32_t st = 0; st < nsteps; ++st) {
+    // faithful device stream after st fills of n particles (rng.py:125)
+    const uint64_t fs = fstate + static_cast<uint64_t>(st) * 7ull * static_cast<uint64_t>(n) * kGamma;
+    for (int64_t k = 0; k < nchunks; ++k) {
+      const int64_t g = st * nchunks + k;  // global chunk sequence number
+      const int b = static_cast<int>(g % nbuf);
+      const int64_t off = b * chunk, lo = k * chunk, cnt = std::min(chunk, n - lo);
+      cudaEvent_t h2d_done = c->ring_ev[3 * b], run_done = c->ring_ev[3 * b + 1],
+                  d2h_done = c->ring_ev[3 * b + 2];
+      if (g >= nbuf) CK(cudaStreamWaitEvent(c->copy, d2h_done, 0));        // slot free
+      if (st > 0) CK(cudaStreamWaitEvent(c->copy, c->host_ev[k], 0));      // host rows landed
+      for (const Row& r : rows)
+        if (r.in) CK(cudaMemcpyAsync(r.dev + off, r.host + lo, sizeof(double) * cnt, cudaMemcpyHostToDevice, c->copy));
+      CK(cudaEventRecord(h2d_done, c->copy));
+      CK(cudaStreamWaitEvent(c->stream, h2d_done, 0));
+      CK(launch_iota(c->ids, off, cnt, first_id + lo, c->stream));
+      rc = c->prec == LT_MET_F64
+               ? run_typed<RecD>(c, ctl, modules, off, off + cnt, step + st, fs, first_id, LT_RUN_RNG_INKERNEL)
+               : run_typed<RecF>(c, ctl, modules, off, off + cnt, step + st, fs, first_id, LT_RUN_RNG_INKERNEL);
+      if (rc) return rc;
+      CK(cudaEventRecord(run_done, c->stream));
+      CK(cudaStreamWaitEvent(c->d2h, run_done, 0));
+      for (const Row& r : rows)
+        if (r.out) CK(cudaMemcpyAsync(r.host + lo, r.dev + off, sizeof(double) * cnt, cudaMemcpyDeviceToHost, c->d2h));
+      CK(cudaEventRecord(d2h_done, c->d2h));
+      CK(cudaEventRecord(c->host_ev[k], c->d2h));
+    }
+  }
+  const int64_t last = static_cast<int64_t>(nsteps) * nchunks - 1;
   CK(cudaEventRecord(c->compute_mark, c->stream));
   c->marked = true;
   if (c->timing) {
-    CK(cudaStreamWaitEvent(c->stream, c->ring_ev[3 * ((nchunks - 1) % nbuf) + 2], 0));
+    CK(cudaStreamWaitEvent(c->stream, c->ring_ev[3 * (last % nbuf) + 2], 0));
     CK(cudaEventRecord(c->ev_stop, c->stream));
     c->timed_once = true;
   }

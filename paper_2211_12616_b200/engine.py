@@ -181,11 +181,12 @@ class Engine:
         self._last_modules = modules
 
     def step_host(self, ctl, ens, cache, step: int, modules: int = ADV_DIFF,
-                  device_id: int = 0, chunk: int = 0) -> None:
-        """One fused step of a HOST ensemble (numpy SoA, ideally in pinned
-        memory — see context.pinned_empty), updated in place: the particles
-        stream through this GPU's store in chunks with H2D, kernel and D2H
-        overlapped (lt_run_host).  Particle i has global id first_id + i."""
+                  device_id: int = 0, chunk: int = 0, steps: int = 1) -> None:
+        """`steps` fused steps (step, step+1, ...) of a HOST ensemble (numpy
+        SoA, ideally in pinned memory — see context.pinned_empty), updated
+        in place: every step streams every particle through this GPU's store
+        in chunks with H2D, kernel and D2H overlapped, and across steps
+        (lt_run_host_steps).  Particle i has global id first_id + i."""
         n = int(ens.np)
         if self.ctx.capacity == 0:
             self.ctx.alloc(min(max(n, 1), 1 << 24), max(self.nq, ens.q.shape[0]))
@@ -194,14 +195,15 @@ class Engine:
             if self.faithful_state is None:
                 self.faithful_state = rng_seed_for(ctl.mpi_rank, device_id)
             fstate = self.faithful_state
-            self.faithful_state = advance_faithful(fstate, n)
+            for _ in range(steps):
+                self.faithful_state = advance_faithful(self.faithful_state, n)
         want = lambda bits: bool(modules & bits)
         self.ctx.run_host(ctl, modules, n, step, self.first_id, ens.time, ens.p, ens.lon, ens.lat,
                           uvwp=cache.uvwp if want(capi.MOD_MESO) else None,
                           iso_var=cache.iso_var if want(capi.MOD_ISOSURF |
                                                         capi.MOD_ISOSURF_INIT) else None,
                           q=ens.q if want(capi.MOD_METEO | capi.MOD_DECAY) else None,
-                          faithful_state=fstate, chunk=chunk)
+                          faithful_state=fstate, chunk=chunk, steps=steps)
         self.sorted = False
 
     def sort(self) -> None:

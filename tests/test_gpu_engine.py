@@ -364,3 +364,43 @@ def test_fast_precision_philox_within_tolerance(eng):
     assert dlon.max() / 360.0 <= 1e-5
     assert np.abs(fast.lat - exact.lat).max() / 180.0 <= 1e-5
     assert (np.abs(fast.p - exact.p) / exact.p).max() <= 1e-5
+
+
+@pytest.mark.parametrize("mode", ["counter", "faithful"])
+def test_host_path_multi_step_call_equals_single_steps(eng, golden_chain, mode):
+    """lt_run_host_steps (K steps per call, pipelined across steps, a ring
+    smaller than the ensemble) == K single-step calls, bit for bit."""
+    engine, ms, _ = eng
+    from paper_2211_12616_b200.context import pinned_empty
+    g = golden_chain
+    base = vars(chain_ctl()).copy()
+    base["rng_mode"] = mode
+    ctl = ms.Control(**{k: v for k, v in base.items() if k in ms.Control.__dataclass_fields__})
+    m0, m1 = snapshot_from(g, "m0"), snapshot_from(g, "m1")
+    outs = []
+    for split in (True, False):
+        ens = _ens(ms, g, "init")
+        n = ens.np
+        rows = {k: pinned_empty(n) for k in ("time", "p", "lon", "lat")}
+        for k, a in rows.items():
+            a[:] = getattr(ens, k)
+        q = pinned_empty((5, n))
+        q[:] = ens.q
+        host = ms.ParticleEnsemble(n, rows["time"], rows["p"], ens.zeta, rows["lon"],
+                                   rows["lat"], q)
+        cache = ms.CacheState(uvwp=pinned_empty((3, n)), iso_var=pinned_empty(n))
+        cache.uvwp[:] = 0.0
+        e = engine.Engine(device=0, first_id=0)
+        e.ctx.alloc(1024, 5)                       # ring of 2 slots of 512
+        e.bind_met(m0, m1)
+        e.load_clim(ms.read_clim(ctl))
+        e.ctx.run_host(ctl, engine.capi.MOD_ISOSURF_INIT, n, 0, 0, host.time, host.p, host.lon,
+                       host.lat, iso_var=cache.iso_var, chunk=512)
+        if split:
+            for step in range(4):
+                e.step_host(ctl, host, cache, step, engine.FULL, chunk=512)
+        else:
+            e.step_host(ctl, host, cache, 0, engine.FULL, chunk=512, steps=4)
+        e.close()
+        outs.append(np.stack([host.lon, host.lat, host.p, host.time, *host.q, *cache.uvwp]))
+    np.testing.assert_array_equal(outs[0], outs[1])
