@@ -507,8 +507,6 @@ int lt_set_home_rows(lt_ctx* c, uint32_t mask) {
   if (mask & ~(LT_HOME_Q | LT_HOME_ZETA | LT_HOME_DT)) return fail(LT_ERR_ARG, "unknown home row bits");
   const uint32_t change = mask ^ c->home_mask;
   if (!change) return LT_OK;
-  if (c->ids && c->home_n == 0)
-    return fail(LT_ERR_STATE, "home order needs an id layout from lt_ids_reset at offset 0");
   if (change & LT_HOME_ZETA)
     if ((rc = convert_row(c, &c->zeta, true, mask & LT_HOME_ZETA))) return rc;
   if (change & LT_HOME_DT)
