@@ -359,11 +359,26 @@ def decay_factor(ctl, dt, q):
     return np.where(dt > 0.0, q * np.exp(-dt / tau), q)
 
 
+def part1by1(x):
+    """Spread the low 16 bits of x to the even bit positions."""
+    x = np.asarray(x, dtype=np.uint64) & np.uint64(0xFFFF)
+    for shift, mask in ((8, 0x00FF00FF), (4, 0x0F0F0F0F), (2, 0x33333333), (1, 0x55555555)):
+        x = (x | (x << np.uint64(shift))) & np.uint64(mask)
+    return x
+
+
 def box_keys(snap: Snapshot, lon, lat, p):
-    """Linear met-cell index ((i*ny)+j)*(nz-1)+k used by the particle sort
-    (new north-star component; pinned through the reference locate)."""
+    """Sort key of the met cell (i, j, k) of each particle (new north-star
+    component; the cell is pinned through the reference locate): the lon/lat
+    column in Z (Morton) order, bits of i above those of j, times (nz-1),
+    plus the level cell k — when that fits 32 bits, else the linear record
+    index ((i*ny)+j)*(nz-1)+k.  Mirrors lt_sort_by_box."""
     i, j, k, _, _, _ = cell_of(snap, lon, lat, p)
-    ny, nz = snap.lats.shape[0], snap.levs.shape[0]
+    nx, ny, nz = snap.lons.shape[0], snap.lats.shape[0], snap.levs.shape[0]
+    top = int((part1by1(nx - 1) << np.uint64(1)) | part1by1(ny - 1)) * (nz - 1) + (nz - 2)
+    if nx <= 65536 and ny <= 65536 and top < 2 ** 32:
+        col = (part1by1(i) << np.uint64(1)) | part1by1(j)
+        return (col * np.uint64(nz - 1) + k.astype(np.uint64)).astype(np.int64)
     return ((i.astype(np.int64) * ny + j) * (nz - 1) + k).astype(np.int64)
 
 

@@ -78,12 +78,12 @@ __global__ void rng_fill_kernel(int mode, uint64_t seed_or_state, int64_t step, 
 template <class Rec>
 __global__ void box_key_kernel(MetView<Rec> m, const double* lon, const double* lat,
                                const double* p, int64_t start, int64_t n, uint32_t* keys,
-                               uint32_t* vals) {
+                               uint32_t* vals, int morton) {
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t s = start + t;
     const Cell c = cell_of(m, lon[s], lat[s], p[s]);
-    keys[t] = c.r00;
+    keys[t] = morton ? box_key_morton(c.i, c.j, c.k, m.nz) : c.r00;
     vals[t] = static_cast<uint32_t>(t);
   }
 }
@@ -203,12 +203,12 @@ cudaError_t launch_rng_fill(int mode, uint64_t seed, int64_t step, int64_t start
 template <class Rec>
 cudaError_t launch_box_keys(const MetView<Rec>& m, const double* lon, const double* lat,
                             const double* p, int64_t start, int64_t n, uint32_t* keys,
-                            uint32_t* vals, cudaStream_t st) {
-  box_key_kernel<Rec><<<grid_for(n), 256, 0, st>>>(m, lon, lat, p, start, n, keys, vals);
+                            uint32_t* vals, int morton, cudaStream_t st) {
+  box_key_kernel<Rec><<<grid_for(n), 256, 0, st>>>(m, lon, lat, p, start, n, keys, vals, morton);
   return cudaGetLastError();
 }
-template cudaError_t launch_box_keys<RecF>(const MetView<RecF>&, const double*, const double*, const double*, int64_t, int64_t, uint32_t*, uint32_t*, cudaStream_t);
-template cudaError_t launch_box_keys<RecD>(const MetView<RecD>&, const double*, const double*, const double*, int64_t, int64_t, uint32_t*, uint32_t*, cudaStream_t);
+template cudaError_t launch_box_keys<RecF>(const MetView<RecF>&, const double*, const double*, const double*, int64_t, int64_t, uint32_t*, uint32_t*, int, cudaStream_t);
+template cudaError_t launch_box_keys<RecD>(const MetView<RecD>&, const double*, const double*, const double*, int64_t, int64_t, uint32_t*, uint32_t*, int, cudaStream_t);
 
 template <class T>
 cudaError_t launch_permute(T* dst, const T* src, const uint32_t* perm, int64_t start, int64_t n,

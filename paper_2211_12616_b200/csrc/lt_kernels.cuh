@@ -26,10 +26,25 @@ cudaError_t launch_pack_nodes(Rec* out, const float4* nodes, int nx, int ny, int
 cudaError_t launch_rng_fill(int mode, uint64_t seed, int64_t step, int64_t start, int64_t end,
                             const uint32_t* ids, double* conv, double* turb, double* meso,
                             cudaStream_t st);
+// Sort key of a met cell: lon/lat columns in Z (Morton) order, levels
+// fastest within a column — neighbouring columns, whose records a cell's
+// corners share, stay close in the sorted order.
+__host__ __device__ inline uint32_t part1by1(uint32_t x) {
+  x &= 0x0000FFFFu;
+  x = (x | (x << 8)) & 0x00FF00FFu;
+  x = (x | (x << 4)) & 0x0F0F0F0Fu;
+  x = (x | (x << 2)) & 0x33333333u;
+  x = (x | (x << 1)) & 0x55555555u;
+  return x;
+}
+__host__ __device__ inline uint32_t box_key_morton(int i, int j, int k, int nz) {
+  return ((part1by1(static_cast<uint32_t>(i)) << 1) | part1by1(static_cast<uint32_t>(j))) *
+             static_cast<uint32_t>(nz - 1) + static_cast<uint32_t>(k);
+}
 template <class Rec>
 cudaError_t launch_box_keys(const MetView<Rec>& m, const double* lon, const double* lat,
                             const double* p, int64_t start, int64_t n, uint32_t* keys,
-                            uint32_t* vals, cudaStream_t st);
+                            uint32_t* vals, int morton, cudaStream_t st);
 constexpr int kRowSet = 4;
 struct RowSet {
   const double* src[kRowSet];

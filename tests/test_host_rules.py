@@ -98,3 +98,28 @@ def test_met_periodic_rule():
     assert met_periodic(part) is part
     ref = orc.close_longitudes(orc.Snapshot.like(met))
     np.testing.assert_array_equal(ref.lons, closed.lons)
+
+
+def test_box_keys_are_a_bijection_of_cells():
+    """The sort key (Morton lon/lat column, level fastest) is injective over
+    cells and orders columns in Z order, levels ascending inside a column."""
+    from paper_2211_12616_b200 import synthetic
+    lons, lats, levs = synthetic.grid(30.0, 20.0, 6)
+    f = synthetic.era5_like(lons, lats, levs)
+    snap = orc.close_longitudes(orc.Snapshot(0.0, lons, lats, levs, f["u"], f["v"], f["w"],
+                                             f["T"]))
+    nx, ny, nz = snap.lons.size, snap.lats.size, snap.levs.size
+    ii, jj, kk = np.meshgrid(np.arange(nx - 1), np.arange(ny - 1), np.arange(nz - 1), indexing="ij")
+    # cell centres -> (i, j, k) through the reference locate, then keys
+    lon = (snap.lons[ii] + snap.lons[ii + 1]) / 2
+    lat = (snap.lats[jj] + snap.lats[jj + 1]) / 2
+    rev = snap.levs[::-1]
+    p = (rev[kk] + rev[kk + 1]) / 2
+    keys = orc.box_keys(snap, lon.ravel(), lat.ravel(), p.ravel())
+    assert np.unique(keys).size == keys.size
+
+    def morton(i, j):
+        return sum(((i >> b) & 1) << (2 * b + 1) | ((j >> b) & 1) << (2 * b) for b in range(16))
+    i, j, k, *_ = orc.cell_of(snap, lon.ravel(), lat.ravel(), p.ravel())
+    brute = np.array([morton(int(a), int(b)) * (nz - 1) + int(c) for a, b, c in zip(i, j, k)])
+    np.testing.assert_array_equal(keys, brute)
