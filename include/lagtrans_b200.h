@@ -204,10 +204,16 @@ int lt_iso_counter(lt_ctx *ctx, int64_t *value, int32_t reset);
    box-sorted: the element of global particle id g sits at index
    g - home_base (home_base = first_id of the last lt_ids_reset, which must
    start at offset 0), so the sort need not move them; kernels reach them
-   through the id row.  lt_set_home_rows converts the current layout. */
+   through the id row.  lt_set_home_rows converts the current layout.
+   With every cold group (Q, ZETA, DT, ISO) in home order, lt_sort_by_box
+   of the whole store defers the row permutation and the next lt_run of the
+   production chain (timesteps + advection + turb + meso + position, drawing
+   in-kernel) applies it while it streams the rows; any other call touching
+   particle rows applies it first. */
 #define LT_HOME_Q    (1u << 0)
 #define LT_HOME_ZETA (1u << 1)
 #define LT_HOME_DT   (1u << 2)
+#define LT_HOME_ISO  (1u << 3)
 int lt_set_home_rows(lt_ctx *ctx, uint32_t mask);
 
 /* box sort: stable radix sort of [start, end) by met0 cell, ids travel along */

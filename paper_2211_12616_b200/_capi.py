@@ -42,7 +42,7 @@ PRECISIONS = {"exact": 0, "fast": 1}
 F_TIME, F_P, F_ZETA, F_LON, F_LAT, F_Q, F_UVWP, F_ISO_VAR, F_DT = range(9)
 F_RND_CONV, F_RND_TURB, F_RND_MESO, F_ID = 9, 10, 11, 12
 
-HOME_Q, HOME_ZETA, HOME_DT = 1, 2, 4
+HOME_Q, HOME_ZETA, HOME_DT, HOME_ISO = 1, 2, 4, 8
 
 MET_F32, MET_F64 = 4, 8
 MET_CLOSE_LON = 1

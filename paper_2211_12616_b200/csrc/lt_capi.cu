@@ -83,7 +83,10 @@ struct lt_ctx {
   int64_t home_base = 0;         // first id of the last lt_ids_reset (offset 0)
   int64_t home_n = 0;            // particles [0, home_n) carry home-order ids
   double* scratch = nullptr;     // cap doubles (ordered copies)
-  double* pool[kRowSet] = {};    // cap doubles each: sort gather targets (swapped with rows)
+  double* pool[8] = {};          // cap doubles each: gather targets (swapped with rows)
+  uint32_t* ids_alt = nullptr;   // cap: the id row a fused sort-and-step writes
+  bool pending = false;          // a box-sort permutation is waiting to be applied
+  int64_t pend_start = 0, pend_n = 0;
   uint32_t* sort_buf = nullptr;  // 4 * cap (keys in/out, vals in/out)
   void* cub_temp = nullptr;
   size_t cub_bytes = 0;
@@ -245,10 +248,11 @@ int ensure_scratch(lt_ctx* c) {
   return LT_OK;
 }
 
-int ensure_pool(lt_ctx* c) {
-  for (double*& r : c->pool)
-    if (!r)
-      if (int rc = alloc_dev(reinterpret_cast<void**>(&r), sizeof(double) * c->cap, "sort pool")) return rc;
+int ensure_pool(lt_ctx* c, int rows = 4) {
+  for (int k = 0; k < rows; ++k)
+    if (!c->pool[k])
+      if (int rc = alloc_dev(reinterpret_cast<void**>(&c->pool[k]), sizeof(double) * c->cap, "sort pool"))
+        return rc;
   return LT_OK;
 }
 
@@ -262,6 +266,8 @@ int ensure_ids(lt_ctx* c) {
 }
 
 }  // namespace
+
+static int settle(lt_ctx* c);  // apply a pending box-sort permutation (below)
 
 extern "C" {
 
@@ -316,6 +322,8 @@ static void free_particles(lt_ctx* c) {
   free_dev(c->ids); c->ids = nullptr;
   c->home_mask = 0; c->home_base = 0; c->home_n = 0;
   for (double*& r : c->pool) { free_dev(r); r = nullptr; }
+  free_dev(c->ids_alt); c->ids_alt = nullptr;
+  c->pending = false;
   free_dev(c->sort_buf); c->sort_buf = nullptr;
   free_dev(c->cub_temp); c->cub_temp = nullptr; c->cub_bytes = 0;
   c->cap = 0;
@@ -409,6 +417,7 @@ int lt_field_devptr(lt_ctx* c, int32_t field, int32_t row, void** dev) {
   int rc = check_ctx(c);
   if (rc) return rc;
   if ((rc = check_particles(c))) return rc;
+  if ((rc = settle(c))) return rc;
   if (field == LT_F_ID) {
     if ((rc = ensure_ids(c))) return rc;
     *dev = c->ids;
@@ -431,6 +440,7 @@ static int slice_check(lt_ctx* c, int64_t off, int64_t cnt, int64_t len) {
 int lt_field_h2d(lt_ctx* c, int32_t field, int32_t row, int64_t off, int64_t cnt, const void* host) {
   int rc = check_ctx(c);
   if (rc || (rc = check_particles(c))) return rc;
+  if ((rc = settle(c))) return rc;
   if (field == LT_F_ID) {
     if ((rc = ensure_ids(c)) || (rc = slice_check(c, off, cnt, c->cap))) return rc;
     if (cnt) CK(cudaMemcpyAsync(c->ids + off, host, 4 * cnt, cudaMemcpyHostToDevice, c->stream));
@@ -446,6 +456,7 @@ int lt_field_h2d(lt_ctx* c, int32_t field, int32_t row, int64_t off, int64_t cnt
 int lt_field_d2h(lt_ctx* c, int32_t field, int32_t row, int64_t off, int64_t cnt, void* host) {
   int rc = check_ctx(c);
   if (rc || (rc = check_particles(c))) return rc;
+  if ((rc = settle(c))) return rc;
   if (field == LT_F_ID) {
     if ((rc = ensure_ids(c)) || (rc = slice_check(c, off, cnt, c->cap))) return rc;
     if (cnt) CK(cudaMemcpyAsync(host, c->ids + off, 4 * cnt, cudaMemcpyDeviceToHost, c->stream));
@@ -463,6 +474,7 @@ int lt_field_d2h(lt_ctx* c, int32_t field, int32_t row, int64_t off, int64_t cnt
 int lt_field_fill(lt_ctx* c, int32_t field, int32_t row, int64_t off, int64_t cnt, double value) {
   int rc = check_ctx(c);
   if (rc || (rc = check_particles(c))) return rc;
+  if ((rc = settle(c))) return rc;
   int64_t len;
   double* p = field_ptr(c, field, row, &len, &rc);
   if (rc || (rc = slice_check(c, off, cnt, len))) return rc;
@@ -473,6 +485,7 @@ int lt_field_fill(lt_ctx* c, int32_t field, int32_t row, int64_t off, int64_t cn
 int lt_ids_reset(lt_ctx* c, int64_t off, int64_t cnt, int64_t first_id) {
   int rc = check_ctx(c);
   if (rc || (rc = check_particles(c))) return rc;
+  if ((rc = settle(c))) return rc;
   if ((rc = ensure_ids(c)) || (rc = slice_check(c, off, cnt, c->cap))) return rc;
   if (first_id < 0 || first_id + cnt > (int64_t(1) << 32))
     return fail(LT_ERR_ARG, "particle ids must fit in 32 bits");
@@ -504,13 +517,17 @@ static int convert_row(lt_ctx* c, double** row, bool separate, bool to_home) {
 int lt_set_home_rows(lt_ctx* c, uint32_t mask) {
   int rc = check_ctx(c);
   if (rc || (rc = check_particles(c))) return rc;
-  if (mask & ~(LT_HOME_Q | LT_HOME_ZETA | LT_HOME_DT)) return fail(LT_ERR_ARG, "unknown home row bits");
+  if ((rc = settle(c))) return rc;
+  if (mask & ~(LT_HOME_Q | LT_HOME_ZETA | LT_HOME_DT | LT_HOME_ISO))
+    return fail(LT_ERR_ARG, "unknown home row bits");
   const uint32_t change = mask ^ c->home_mask;
   if (!change) return LT_OK;
   if (change & LT_HOME_ZETA)
     if ((rc = convert_row(c, &c->zeta, true, mask & LT_HOME_ZETA))) return rc;
   if (change & LT_HOME_DT)
     if ((rc = convert_row(c, &c->dt, true, mask & LT_HOME_DT))) return rc;
+  if (change & LT_HOME_ISO)
+    if ((rc = convert_row(c, &c->iso_var, true, mask & LT_HOME_ISO))) return rc;
   if (change & LT_HOME_Q)
     for (int k = 0; k < c->nq; ++k) {
       double* r = c->q + static_cast<int64_t>(k) * c->cap;
@@ -714,8 +731,25 @@ int lt_clim_load(lt_ctx* c, int32_t nlat, int32_t np_, const double* lat_grid,
 extern "C++" {
 template <class Rec>
 static int run_typed(lt_ctx* c, const lt_control* ctl, uint32_t modules, int64_t start,
-                     int64_t end, int64_t step, uint64_t fstate, int64_t fbase, uint32_t flags) {
+                     int64_t end, int64_t step, uint64_t fstate, int64_t fbase, uint32_t flags,
+                     bool fuse_perm = false) {
   StepArgs<Rec> a;
+  a.perm = nullptr;
+  a.perm_start = 0;
+  a.o_time = a.o_p = a.o_lon = a.o_lat = nullptr;
+  a.o_uvwp[0] = a.o_uvwp[1] = a.o_uvwp[2] = nullptr;
+  a.o_ids = nullptr;
+  if (fuse_perm) {  // apply the pending sort on the fly: hot rows into the pool
+    if (int rc = ensure_pool(c, 7)) return rc;
+    if (!c->ids_alt)
+      if (int rc = alloc_dev(reinterpret_cast<void**>(&c->ids_alt), sizeof(uint32_t) * c->cap, "ids"))
+        return rc;
+    a.perm = c->sort_buf + 3 * c->cap;
+    a.perm_start = c->pend_start;
+    a.o_time = c->pool[0]; a.o_p = c->pool[1]; a.o_lon = c->pool[2]; a.o_lat = c->pool[3];
+    for (int k = 0; k < 3; ++k) a.o_uvwp[k] = c->pool[4 + k];
+    a.o_ids = c->ids_alt;
+  }
   a.time = c->time; a.p = c->p; a.lon = c->lon; a.lat = c->lat; a.dt = c->dt;
   for (int k = 0; k < 3; ++k) a.uvwp[k] = c->uvwp[k];
   a.iso_var = c->iso_var; a.q = c->q;
@@ -747,6 +781,13 @@ static int run_typed(lt_ctx* c, const lt_control* ctl, uint32_t modules, int64_t
     std::memset(&a.clim, 0, sizeof(a.clim));
   }
   CK(launch_step<Rec>(a, c->stream));
+  if (fuse_perm) {  // the pool rows now hold the sorted state
+    std::swap(c->time, c->pool[0]); std::swap(c->p, c->pool[1]);
+    std::swap(c->lon, c->pool[2]); std::swap(c->lat, c->pool[3]);
+    for (int k = 0; k < 3; ++k) std::swap(c->uvwp[k], c->pool[4 + k]);
+    std::swap(c->ids, c->ids_alt);
+    c->pending = false;
+  }
   return LT_OK;
 }
 }  // extern C++
@@ -763,10 +804,19 @@ int lt_run(lt_ctx* c, const lt_control* ctl, uint32_t modules, int64_t start, in
   if ((flags & LT_RUN_RNG_INKERNEL) && ctl->rng_mode == RNG_FAITHFUL &&
       (modules & (M_TURB | M_MESO | M_CONVECTION)) && c->ids == nullptr && fbase > start)
     return fail(LT_ERR_ARG, "faithful base beyond range start");
+  // a pending box sort rides along with a whole-store production step;
+  // anything else applies it first
+  bool fuse = false;
+  if (c->pending) {
+    fuse = perm_capable(modules, flags, ctl->rng_mode) && start == 0 && end == c->cap &&
+           c->pend_start == 0 && c->pend_n == c->cap;
+    if (!fuse && (rc = settle(c))) return rc;
+  }
   if (c->timing) CK(cudaEventRecord(c->ev_start, c->stream));
   if (end > start) {
-    rc = c->prec == LT_MET_F64 ? run_typed<RecD>(c, ctl, modules, start, end, step, fstate, fbase, flags)
-                               : run_typed<RecF>(c, ctl, modules, start, end, step, fstate, fbase, flags);
+    rc = c->prec == LT_MET_F64
+             ? run_typed<RecD>(c, ctl, modules, start, end, step, fstate, fbase, flags, fuse)
+             : run_typed<RecF>(c, ctl, modules, start, end, step, fstate, fbase, flags, fuse);
     if (rc) return rc;
   }
   CK(cudaEventRecord(c->compute_mark, c->stream));
@@ -796,6 +846,7 @@ int lt_run_host_steps(lt_ctx* c, const lt_control* ctl, uint32_t modules, int64_
                       int64_t chunk) {
   int rc = check_ctx(c);
   if (rc || (rc = check_particles(c))) return rc;
+  if ((rc = settle(c))) return rc;
   if (!io || !io->time || !io->p || !io->lon || !io->lat)
     return fail(LT_ERR_ARG, "host SoA needs time, p, lon and lat");
   if (n < 0) return fail(LT_ERR_ARG, "negative particle count");
@@ -901,6 +952,7 @@ int lt_run_host_steps(lt_ctx* c, const lt_control* ctl, uint32_t modules, int64_
 int lt_rng_fill(lt_ctx* c, int32_t mode, uint64_t seed, int64_t step, int64_t start, int64_t end) {
   int rc = check_ctx(c);
   if (rc || (rc = check_particles(c))) return rc;
+  if ((rc = settle(c))) return rc;
   if (!c->rnd_conv) return fail(LT_ERR_STATE, "context allocated without a random batch");
   if (!(0 <= start && start <= end && end <= c->cap))
     return fail(LT_ERR_RANGE, "range [%lld, %lld) outside ensemble of %lld particles",
@@ -986,14 +1038,26 @@ static int sort_typed(lt_ctx* c, int64_t start, int64_t end) {
   }
   size_t have = c->cub_bytes;
   CK(sort_pairs(c->cub_temp, have, keys_in, keys_out, vals_in, vals_out, n, bits, c->stream));
+  return LT_OK;
+}
+}  // extern C++
+
+extern "C++" {
+// The permutation of the last sort (sort_buf vals_out) applied to the rows:
+// new slot start + t takes old slot start + perm[t].
+static int apply_perm(lt_ctx* c, int64_t start, int64_t n) {
+  uint32_t* keys_in = c->sort_buf;
+  const uint32_t* vals_out = c->sort_buf + 3 * c->cap;
+  const int64_t end = start + n;
   // Permute every per-particle row, kRowSet rows per launch into the pool
   // rows.  Separately allocated rows covering the whole store swap pointers
   // with their pool row (no copy back); the q block and partial ranges copy
   // the gathered slice back.
   if (int rc = ensure_pool(c)) return rc;
   const bool whole = start == 0 && end == c->cap;
-  std::vector<double**> rows = {&c->time, &c->p, &c->lon, &c->lat, &c->iso_var,
+  std::vector<double**> rows = {&c->time, &c->p, &c->lon, &c->lat,
                                 &c->uvwp[0], &c->uvwp[1], &c->uvwp[2]};
+  if (!(c->home_mask & LT_HOME_ISO)) rows.push_back(&c->iso_var);
   if (!(c->home_mask & LT_HOME_ZETA)) rows.push_back(&c->zeta);
   if (!(c->home_mask & LT_HOME_DT)) rows.push_back(&c->dt);
   for (size_t g = 0; g < rows.size(); g += kRowSet) {
@@ -1018,11 +1082,18 @@ static int sort_typed(lt_ctx* c, int64_t start, int64_t end) {
   CK(cudaMemcpyAsync(c->ids + start, keys_in + start, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, c->stream));
   return LT_OK;
 }
+
+static int settle(lt_ctx* c) {
+  if (!c->pending) return LT_OK;
+  c->pending = false;
+  return apply_perm(c, c->pend_start, c->pend_n);
+}
 }  // extern C++
 
 int lt_sort_by_box(lt_ctx* c, int64_t start, int64_t end) {
   int rc = check_ctx(c);
   if (rc || (rc = check_particles(c))) return rc;
+  if ((rc = settle(c))) return rc;
   if (!(0 <= start && start <= end && end <= c->cap))
     return fail(LT_ERR_RANGE, "range [%lld, %lld) outside ensemble of %lld particles",
                 (long long)start, (long long)end, (long long)c->cap);
@@ -1039,6 +1110,15 @@ int lt_sort_by_box(lt_ctx* c, int64_t start, int64_t end) {
   if (c->timing) CK(cudaEventRecord(c->ev_start, c->stream));
   rc = c->prec == LT_MET_F64 ? sort_typed<RecD>(c, start, end) : sort_typed<RecF>(c, start, end);
   if (rc) return rc;
+  // With every cold row in particle order, the next production-chain step
+  // can apply the permutation while it streams the hot rows (lt_run); any
+  // other access settles it first.
+  const uint32_t cold = LT_HOME_Q | LT_HOME_ZETA | LT_HOME_DT | LT_HOME_ISO;
+  c->pend_start = start;
+  c->pend_n = end - start;
+  c->pending = true;
+  if (!(start == 0 && end == c->cap && (c->home_mask & cold) == cold))
+    if ((rc = settle(c))) return rc;
   CK(cudaEventRecord(c->compute_mark, c->stream));
   c->marked = true;
   if (c->timing) { CK(cudaEventRecord(c->ev_stop, c->stream)); c->timed_once = true; }
@@ -1049,6 +1129,7 @@ static int ordered_copy(lt_ctx* c, int32_t field, int32_t row, int64_t off, int6
                         int64_t first_id, void* host, bool to_host) {
   int rc = check_ctx(c);
   if (rc || (rc = check_particles(c))) return rc;
+  if ((rc = settle(c))) return rc;
   if (field == LT_F_ID || field == LT_F_RND_CONV || field == LT_F_RND_TURB || field == LT_F_RND_MESO)
     return fail(LT_ERR_ARG, "ordered copies apply to per-particle state fields only");
   int64_t len;
@@ -1059,7 +1140,7 @@ static int ordered_copy(lt_ctx* c, int32_t field, int32_t row, int64_t off, int6
                    : lt_field_h2d(c, field, row, off, cnt, host);
   }
   const uint32_t group = field == LT_F_Q ? LT_HOME_Q : field == LT_F_ZETA ? LT_HOME_ZETA
-                         : field == LT_F_DT ? LT_HOME_DT : 0u;
+                         : field == LT_F_DT ? LT_HOME_DT : field == LT_F_ISO_VAR ? LT_HOME_ISO : 0u;
   if (group & c->home_mask) {  // particle order already: contiguous at id - home_base
     const int64_t at = first_id - c->home_base;
     if ((rc = slice_check(c, at, cnt, len))) return rc;
@@ -1100,6 +1181,7 @@ int lt_field_h2d_ordered(lt_ctx* c, int32_t field, int32_t row, int64_t off, int
 int lt_grid_counts(lt_ctx* c, int32_t nx, int32_t ny, int64_t start, int64_t end, int64_t* counts) {
   int rc = check_ctx(c);
   if (rc || (rc = check_particles(c))) return rc;
+  if ((rc = settle(c))) return rc;
   if (nx < 1 || ny < 1) return fail(LT_ERR_ARG, "grid needs nx, ny >= 1");
   if (!(0 <= start && start <= end && end <= c->cap))
     return fail(LT_ERR_RANGE, "range [%lld, %lld) outside ensemble of %lld particles",
@@ -1124,6 +1206,7 @@ int lt_group_stats(lt_ctx* c, int32_t slot, int64_t start, int64_t end, int64_t 
                    int64_t* ngroups, int64_t* gid, int64_t* count, double* mean, double* std_) {
   int rc = check_ctx(c);
   if (rc || (rc = check_particles(c))) return rc;
+  if ((rc = settle(c))) return rc;
   if (slot < 0 || slot >= c->nq)
     return fail(LT_ERR_ARG, "ens_group_slot %d is not a valid quantity slot", slot);
   if (!(0 <= start && start <= end && end <= c->cap))

@@ -79,6 +79,7 @@ cudaError_t group_stats(const double* lon, const double* lat, const double* p, c
 
 template <class Rec>
 cudaError_t launch_step(const StepArgs<Rec>& a, cudaStream_t st);
+bool perm_capable(uint32_t modules, uint32_t flags, int rng_mode);
 
 cudaError_t sort_pairs(void* temp, size_t& temp_bytes, const uint32_t* keys_in,
                        uint32_t* keys_out, const uint32_t* vals_in, uint32_t* vals_out,

@@ -9,7 +9,7 @@ namespace lt {
 constexpr uint32_t kChainAdv = M_TIMESTEPS | M_ADVECTION | M_POSITION;
 constexpr uint32_t kChainAdvDiff = M_TIMESTEPS | M_ADVECTION | M_TURB | M_MESO | M_POSITION;
 
-template <class Rec, uint32_t FIXED, bool FAST, int RM>
+template <class Rec, uint32_t FIXED, bool FAST, int RM, bool PERM = false>
 static cudaError_t launch_fixed(const StepArgs<Rec>& a, cudaStream_t st) {
   static int blocks_per_sm = 0;
   static int sms = 0;
@@ -17,7 +17,7 @@ static cudaError_t launch_fixed(const StepArgs<Rec>& a, cudaStream_t st) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, step_kernel<Rec, FIXED, FAST, RM>, LT_STEP_BLOCK, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, step_kernel<Rec, FIXED, FAST, RM, PERM>, LT_STEP_BLOCK, 0);
     if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
   const int64_t n = a.end - a.start;
@@ -28,13 +28,19 @@ static cudaError_t launch_fixed(const StepArgs<Rec>& a, cudaStream_t st) {
 #endif
   const int64_t cap = static_cast<int64_t>(sms) * blocks_per_sm * LT_GRID_WAVES;
   if (grid > cap) grid = cap;
-  step_kernel<Rec, FIXED, FAST, RM><<<static_cast<unsigned>(grid), LT_STEP_BLOCK, 0, st>>>(a);
+  step_kernel<Rec, FIXED, FAST, RM, PERM><<<static_cast<unsigned>(grid), LT_STEP_BLOCK, 0, st>>>(a);
   return cudaGetLastError();
 }
 
 template <class Rec, bool FAST>
 static cudaError_t launch_prec(const StepArgs<Rec>& a, cudaStream_t st) {
-  // the production chain gets its in-kernel generator fixed at compile time
+  // the production chain gets its in-kernel generator fixed at compile time;
+  // with a pending box-sort permutation it applies it on the fly
+  if (a.perm) {
+    if (a.ctl.rng_mode == RNG_COUNTER) return launch_fixed<Rec, kChainAdvDiff, FAST, RNG_COUNTER, true>(a, st);
+    if (a.ctl.rng_mode == RNG_PHILOX) return launch_fixed<Rec, kChainAdvDiff, FAST, RNG_PHILOX, true>(a, st);
+    return launch_fixed<Rec, kChainAdvDiff, FAST, RNG_FAITHFUL, true>(a, st);
+  }
   if (a.modules == kChainAdvDiff && (a.flags & F_RNG_INKERNEL)) {
     if (a.ctl.rng_mode == RNG_COUNTER) return launch_fixed<Rec, kChainAdvDiff, FAST, RNG_COUNTER>(a, st);
     if (a.ctl.rng_mode == RNG_PHILOX) return launch_fixed<Rec, kChainAdvDiff, FAST, RNG_PHILOX>(a, st);
@@ -43,6 +49,14 @@ static cudaError_t launch_prec(const StepArgs<Rec>& a, cudaStream_t st) {
   if (a.modules == kChainAdvDiff) return launch_fixed<Rec, kChainAdvDiff, FAST, -1>(a, st);
   if (a.modules == kChainAdv) return launch_fixed<Rec, kChainAdv, FAST, -1>(a, st);
   return launch_fixed<Rec, 0, FAST, -1>(a, st);
+}
+
+// launches that can apply a pending box-sort permutation on the fly: the
+// production chain (it reads and writes every hot row) with a compile-time
+// in-kernel generator
+bool perm_capable(uint32_t modules, uint32_t flags, int rng_mode) {
+  return modules == kChainAdvDiff && (flags & F_RNG_INKERNEL) &&
+         (rng_mode == RNG_COUNTER || rng_mode == RNG_PHILOX || rng_mode == RNG_FAITHFUL);
 }
 
 template <class Rec>

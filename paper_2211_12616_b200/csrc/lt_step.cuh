@@ -27,6 +27,14 @@ struct StepArgs {
   const uint32_t* ids;  // global particle index per slot, or null (= slot)
   uint32_t home_mask;   // HOME_* row groups kept in particle order (index id - home_base)
   int64_t home_base;
+  // pending box-sort permutation (PERM kernels): slot s of the new order
+  // holds old slot perm_start + perm[s - perm_start]; the hot rows and ids
+  // are gathered through it and written to the o_* rows
+  const uint32_t* perm;
+  int64_t perm_start;
+  double *o_time, *o_p, *o_lon, *o_lat;
+  double* o_uvwp[3];
+  uint32_t* o_ids;
   const double* rnd_conv;
   const double* rnd_turb;
   const double* rnd_meso;
@@ -149,13 +157,15 @@ __device__ __forceinline__ void draws(const StepArgs<Rec>& a, int64_t s, uint64_
   }
 }
 
-// index of slot s in a row group that may be kept in particle order
+// index of a particle in a row group that may be kept in particle order:
+// slot s (source slot `src` of a pending permutation) or its id - home_base
 template <class Rec>
-__device__ __forceinline__ int64_t row_index(const StepArgs<Rec>& a, int64_t s, uint32_t group) {
-  return (a.home_mask & group) && a.ids ? static_cast<int64_t>(a.ids[s]) - a.home_base : s;
+__device__ __forceinline__ int64_t row_index(const StepArgs<Rec>& a, int64_t s, int64_t src,
+                                             uint32_t group) {
+  return (a.home_mask & group) && a.ids ? static_cast<int64_t>(a.ids[src]) - a.home_base : s;
 }
 
-template <class Rec, uint32_t FIXED, bool FAST, int RM>
+template <class Rec, uint32_t FIXED, bool FAST, int RM, bool PERM>
 __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel(const StepArgs<Rec> a) {
   using O = Ops<Rec, FAST>;
   const uint32_t mods = FIXED ? FIXED : a.modules;
@@ -170,10 +180,13 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
   unsigned long long nonconv = 0;
 
   for (int64_t s = s_lo + threadIdx.x; s < s_hi; s += stride) {
+    // PERM: this slot's particle comes from old slot `src` (box sort applied
+    // on the fly: gathered reads, coalesced writes to the o_* rows)
+    const int64_t src = PERM ? a.perm_start + a.perm[s - a.perm_start] : s;
     // stage the next particle's state rows into L2 while this one runs
     // (costs no registers; the loads below then hit L2 instead of HBM)
 #ifndef LT_NO_PREFETCH
-    if (s + stride < s_hi) {
+    if (!PERM && s + stride < s_hi) {
       const int64_t nx = s + stride;
       prefetch_l2(a.time + nx); prefetch_l2(a.lon + nx); prefetch_l2(a.lat + nx);
       prefetch_l2(a.p + nx);
@@ -183,17 +196,17 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
       if (a.ids && (mods & (M_TURB | M_MESO | M_CONVECTION))) prefetch_l2(a.ids + nx);
     }
 #endif
-    double time = ld_state(a.time + s), lon = ld_state(a.lon + s), lat = ld_state(a.lat + s),
-           p = ld_state(a.p + s);
+    double time = ld_state(a.time + src), lon = ld_state(a.lon + src), lat = ld_state(a.lat + src),
+           p = ld_state(a.p + src);
 
     // physics.py:82-88 (module_timesteps)
     double dt;
     if ((mods & M_TIMESTEPS) || !(a.flags & F_DT_ARRAY)) {
       dt = fmin(ctl.dt_model, ctl.t_stop - time);
       dt = fmin(fmax(dt, 0.0), ctl.dt_model);
-      if ((mods & M_TIMESTEPS) && (a.flags & F_WRITE_DT)) a.dt[row_index(a, s, HOME_DT)] = dt;
+      if ((mods & M_TIMESTEPS) && (a.flags & F_WRITE_DT)) a.dt[row_index(a, s, src, HOME_DT)] = dt;
     } else {
-      dt = a.dt[row_index(a, s, HOME_DT)];
+      dt = a.dt[row_index(a, s, src, HOME_DT)];
     }
     const bool act = dt > 0.0;
 
@@ -204,7 +217,7 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
     const bool want_meso = (mods & M_MESO) && ctl.turb_meso != 0.0;
     const bool want_conv = (mods & M_CONVECTION) && ctl.conv_prob != 0.0;
     const uint64_t gid = (RM >= 0 || (a.flags & F_RNG_INKERNEL)) && (want_turb || want_meso || want_conv)
-                             ? (a.ids ? static_cast<uint64_t>(a.ids[s]) : static_cast<uint64_t>(s))
+                             ? (a.ids ? static_cast<uint64_t>(a.ids[src]) : static_cast<uint64_t>(s))
                              : 0ull;
 #ifndef LT_LATE_DRAWS
     // fast path with a compile-time generator: the six normals are pure ALU
@@ -236,11 +249,11 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
     // physics.py:225-235 (module_isosurf_init)
     if ((mods & M_ISOSURF_INIT) && ctl.isosurf_mode != ISO_OFF) {
       if (ctl.isosurf_mode == ISO_PRESSURE) {
-        a.iso_var[s] = p;
+        a.iso_var[row_index(a, s, src, HOME_ISO)] = p;
       } else {
         double v[4];
         O::sample(a.met, time, lon, lat, p, 8, v);
-        a.iso_var[s] = v[3] * pow(1000.0 / p, kKappa);
+        a.iso_var[row_index(a, s, src, HOME_ISO)] = v[3] * pow(1000.0 / p, kKappa);
       }
     }
 
@@ -313,8 +326,8 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
 #pragma unroll
       for (int f = 0; f < 3; ++f) {
         const double sigma = ctl.turb_meso * O::spread(q, f);
-        pert[f] = r * ld_state(a.uvwp[f] + s) + amp * sigma * xm[f];
-        st_state(a.uvwp[f] + s, pert[f]);
+        pert[f] = r * ld_state(a.uvwp[f] + src) + amp * sigma * xm[f];
+        st_state((PERM ? a.o_uvwp[f] : a.uvwp[f]) + s, pert[f]);
       }
       const double nlon = lon + O::over_cos(pert[0] * dt * kDegPerM, lat);
       lat = lat + pert[1] * dt * kDegPerM;
@@ -343,16 +356,16 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
     // decay (new module): q[slot] *= exp(-dt / tau) while active
     if ((mods & M_DECAY) && ctl.decay_tau > 0.0 && act && ctl.decay_slot >= 0 &&
         ctl.decay_slot < a.nq) {
-      double* qs = a.q + static_cast<int64_t>(ctl.decay_slot) * a.cap + row_index(a, s, HOME_Q);
+      double* qs = a.q + static_cast<int64_t>(ctl.decay_slot) * a.cap + row_index(a, s, src, HOME_Q);
       *qs = *qs * exp(-dt / ctl.decay_tau);
     }
 
     // physics.py:238-264 (module_isosurf): applies to every particle
     if ((mods & M_ISOSURF) && ctl.isosurf_mode != ISO_OFF) {
       if (ctl.isosurf_mode == ISO_PRESSURE) {
-        p = a.iso_var[s];
+        p = a.iso_var[row_index(a, s, src, HOME_ISO)];
       } else {
-        const double theta0 = a.iso_var[s];
+        const double theta0 = a.iso_var[row_index(a, s, src, HOME_ISO)];
         bool pending = true;
         for (int it = 0; it < 10 && pending; ++it) {
           double v[4];
@@ -388,7 +401,7 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
     if (mods & M_METEO) {
       double v[4];
       O::sample(a.met, time, lon, lat, p, 11, v);
-      const int64_t qi = row_index(a, s, HOME_Q);
+      const int64_t qi = row_index(a, s, src, HOME_Q);
       a.q[qi] = v[3];
       a.q[a.cap + qi] = v[0];
       a.q[2 * a.cap + qi] = v[1];
@@ -397,10 +410,24 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
     }
 
     if (mods & (M_ADVECTION | M_TURB | M_MESO | M_CONVECTION | M_SEDI | M_ISOSURF | M_POSITION)) {
-      st_state(a.p + s, p);
-      st_state(a.lon + s, lon);
-      st_state(a.lat + s, lat);
-      if (mods & M_ADVECTION) st_state(a.time + s, time);
+      st_state((PERM ? a.o_p : a.p) + s, p);
+      st_state((PERM ? a.o_lon : a.lon) + s, lon);
+      st_state((PERM ? a.o_lat : a.lat) + s, lat);
+      if (mods & M_ADVECTION) st_state((PERM ? a.o_time : a.time) + s, time);
+    }
+    if (PERM) {  // every hot row moves with its particle, touched this step or not
+      if (!(mods & (M_ADVECTION | M_TURB | M_MESO | M_CONVECTION | M_SEDI | M_ISOSURF |
+                    M_POSITION))) {
+        st_state(a.o_p + s, p);
+        st_state(a.o_lon + s, lon);
+        st_state(a.o_lat + s, lat);
+      }
+      if (!(mods & M_ADVECTION)) st_state(a.o_time + s, time);
+      if (!(want_meso && act)) {
+#pragma unroll
+        for (int f = 0; f < 3; ++f) st_state(a.o_uvwp[f] + s, ld_state(a.uvwp[f] + src));
+      }
+      a.o_ids[s] = a.ids[src];
     }
   }
 

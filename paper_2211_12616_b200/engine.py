@@ -208,11 +208,17 @@ class Engine:
 
     def sort(self) -> None:
         """Stable box sort of the shard.  Rows the stepping modules do not
-        touch (zeta, dt, and q unless meteo/decay run) stay in particle
-        order, so the sort moves only the rows the step kernel streams."""
+        touch (zeta, dt; q unless meteo/decay run; iso_var unless isosurf
+        runs) stay in particle order, so the sort moves only the rows the step
+        kernel streams — and with all of those cold, the next production-chain
+        step applies the permutation itself while it streams them
+        (lt_sort_by_box defers it, lt_run fuses it)."""
+        last = getattr(self, "_last_modules", 0)
         home = capi.HOME_ZETA | capi.HOME_DT
-        if not (getattr(self, "_last_modules", 0) & (capi.MOD_METEO | capi.MOD_DECAY)):
-            home |= capi.HOME_Q   # (a later meteo/decay step still works, via the ids)
+        if not (last & (capi.MOD_METEO | capi.MOD_DECAY)):
+            home |= capi.HOME_Q      # (a later meteo/decay step still works, via the ids)
+        if not (last & (capi.MOD_ISOSURF | capi.MOD_ISOSURF_INIT)):
+            home |= capi.HOME_ISO
         self.ctx.set_home_rows(home)
         self.ctx.sort_by_box(0, self.n)
         self.sorted = True
