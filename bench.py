@@ -544,11 +544,13 @@ def main():
                          f"same {wl} met grid ({wall:.1f} s)"}
 
     # launches of our kernels in the headline timed region: one fused step
-    # per step; per sort: keys 1 + CUB radix sort 6 + row gathers (8 hot rows,
-    # plus the q rows when meteo/decay keep them in slot order, 4 per launch)
-    # + ids 1; per streamed snapshot: one packing kernel
+    # per step; per sort: keys 1 + CUB radix sort 6, plus — unless every cold
+    # row is in particle order and the next step applies the permutation —
+    # row gathers (8 hot rows, plus the q rows when meteo/decay keep them in
+    # slot order, 4 per launch) + ids 1; per streamed snapshot: one packing kernel
     q_hot = any(m in cfg["chain"] for m in ("meteo", "decay"))
-    per_sort = 1 + 6 + 2 + (-(-ctl.nq // 4) if q_hot else 0) + 1
+    deferred = not q_hot and "isosurf" not in cfg["chain"]
+    per_sort = 1 + 6 + (0 if deferred else 2 + (-(-ctl.nq // 4) if q_hot else 0) + 1)
     launches = args.steps + sorts_timed * per_sort + rots
     if rank == 0:
         print(json.dumps({
