@@ -50,18 +50,23 @@ def build(force: bool = False, verbose: bool = False, outdir: Path | None = None
     if not force and outdir is None and not defines and not _stale():
         return LIB
     libdir.mkdir(parents=True, exist_ok=True)
-    objs = []
-    log = []
-    for src in SOURCES:
+
+    def compile_one(src):
         obj = libdir / (Path(src).stem + ".o")
         cmd = [nvcc(), *ARCH, *FLAGS, *[f"-D{d}" for d in defines],
                "-I", str(PKG.parent / "include"), "-c",
                str(CSRC / src), "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
-        log.append(r.stdout + r.stderr)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n{r.stderr}")
-        objs.append(str(obj))
+        return str(obj), r.stdout + r.stderr
+
+    # the translation units compile independently: build them in parallel
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(len(SOURCES)) as pool:
+        results = list(pool.map(compile_one, SOURCES))
+    objs = [o for o, _ in results]
+    log = [text for _, text in results]
     tmp = lib.with_suffix(".so.tmp")
     cmd = [nvcc(), *ARCH, "-shared", "--cudart", "static", "-o", str(tmp), *objs, "-lpthread"]
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -8,6 +8,9 @@ namespace lt {
 // module sets compiled as their own specialisation (dead modules removed)
 constexpr uint32_t kChainAdv = M_TIMESTEPS | M_ADVECTION | M_POSITION;
 constexpr uint32_t kChainAdvDiff = M_TIMESTEPS | M_ADVECTION | M_TURB | M_MESO | M_POSITION;
+// cfg4's plume chain and the full chain (engine.FULL), fp32 met store only
+constexpr uint32_t kChainPlume = kChainAdvDiff | M_SEDI | M_DECAY;
+constexpr uint32_t kChainFull = kChainAdvDiff | M_CONVECTION | M_SEDI | M_DECAY | M_ISOSURF | M_METEO;
 
 template <class Rec, uint32_t FIXED, bool FAST, int RM, bool PERM = false>
 static cudaError_t launch_fixed(const StepArgs<Rec>& a, cudaStream_t st) {
@@ -45,6 +48,17 @@ static cudaError_t launch_prec(const StepArgs<Rec>& a, cudaStream_t st) {
     if (a.ctl.rng_mode == RNG_COUNTER) return launch_fixed<Rec, kChainAdvDiff, FAST, RNG_COUNTER>(a, st);
     if (a.ctl.rng_mode == RNG_PHILOX) return launch_fixed<Rec, kChainAdvDiff, FAST, RNG_PHILOX>(a, st);
     if (a.ctl.rng_mode == RNG_FAITHFUL) return launch_fixed<Rec, kChainAdvDiff, FAST, RNG_FAITHFUL>(a, st);
+  }
+  if constexpr (sizeof(Rec) == sizeof(RecF)) {
+    if ((a.flags & F_RNG_INKERNEL) && (a.modules == kChainPlume || a.modules == kChainFull)) {
+      const bool full = a.modules == kChainFull;
+      if (a.ctl.rng_mode == RNG_PHILOX)
+        return full ? launch_fixed<Rec, kChainFull, FAST, RNG_PHILOX>(a, st)
+                    : launch_fixed<Rec, kChainPlume, FAST, RNG_PHILOX>(a, st);
+      if (a.ctl.rng_mode == RNG_COUNTER)
+        return full ? launch_fixed<Rec, kChainFull, FAST, RNG_COUNTER>(a, st)
+                    : launch_fixed<Rec, kChainPlume, FAST, RNG_COUNTER>(a, st);
+    }
   }
   if (a.modules == kChainAdvDiff) return launch_fixed<Rec, kChainAdvDiff, FAST, -1>(a, st);
   if (a.modules == kChainAdv) return launch_fixed<Rec, kChainAdv, FAST, -1>(a, st);

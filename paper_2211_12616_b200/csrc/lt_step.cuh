@@ -91,6 +91,8 @@ struct Ops {
   }
   template <class T>
   __device__ static double spread(const CornersT<T>& q, int f) { return corner_std(q, f); }
+  // x^e (isosurface potential temperature, physics.py:233-234, 256-257)
+  __device__ static double power(double x, double e) { return pow(x, e); }
   __device__ static void normals(uint64_t seed, int64_t step, uint64_t gid, int stream, double z[3]) {
     counter_normals(seed, step, gid, stream, z);
   }
@@ -112,6 +114,9 @@ struct Ops<RecF, true> {
     return col * (m.nz - 1) + (m.nz - 2 - locate_fast(m.lev, p, frev));
   }
   __device__ static double spread(const CornersT<float>& q, int f) { return corner_std_f(q, f); }
+  __device__ static double power(double x, double e) {
+    return static_cast<double>(exp2f(static_cast<float>(e) * __log2f(static_cast<float>(x))));
+  }
   __device__ static void normals(uint64_t seed, int64_t step, uint64_t gid, int stream, double z[3]) {
     counter_normals_fast(seed, step, gid, stream, z);
   }
@@ -253,7 +258,7 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
       } else {
         double v[4];
         O::sample(a.met, time, lon, lat, p, 8, v);
-        a.iso_var[row_index(a, s, src, HOME_ISO)] = v[3] * pow(1000.0 / p, kKappa);
+        a.iso_var[row_index(a, s, src, HOME_ISO)] = v[3] * O::power(1000.0 / p, kKappa);
       }
     }
 
@@ -370,7 +375,7 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
         for (int it = 0; it < 10 && pending; ++it) {
           double v[4];
           O::sample(a.met, time, lon, lat, p, 8, v);
-          const double pn = 1000.0 * pow(v[3] / theta0, kInvKappa);
+          const double pn = 1000.0 * O::power(v[3] / theta0, kInvKappa);
           const double dp = pn - p;
           p = pn;
           pending = fabs(dp) >= 0.1;

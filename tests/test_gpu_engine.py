@@ -404,3 +404,30 @@ def test_host_path_multi_step_call_equals_single_steps(eng, golden_chain, mode):
         e.close()
         outs.append(np.stack([host.lon, host.lat, host.p, host.time, *host.q, *cache.uvwp]))
     np.testing.assert_array_equal(outs[0], outs[1])
+
+
+def test_fast_full_chain_within_tolerance(eng, golden_chain):
+    """All nine modules (theta isosurface, convection, sedimentation,
+    meteo, decay) with the fast kernels against the exact ones over the
+    50-step golden chain."""
+    engine, ms, _ = eng
+    g = golden_chain
+    base = vars(chain_ctl()).copy()
+    base.update(decay_tau=86400.0, decay_slot=4)
+    exact_ctl = ms.Control(**{k: v for k, v in base.items() if k in ms.Control.__dataclass_fields__})
+    fast_ctl = ms.Control(**{**vars(exact_ctl), "precision": "fast"})
+    ex, _ = _run_chain(engine, ms, g, exact_ctl, 50, shards=1, sort_every=10)
+    fa, _ = _run_chain(engine, ms, g, fast_ctl, 50, shards=1, sort_every=10)
+    dlon = np.abs((fa.lon - ex.lon + 180.0) % 360.0 - 180.0) / 360.0
+    dlat = np.abs(fa.lat - ex.lat) / 180.0
+    dp = np.abs(fa.p - ex.p) / ex.p
+    print("full chain fast-vs-exact: max dlon %.2e dlat %.2e dp %.2e; dp>1e-5: %d of %d"
+          % (dlon.max(), dlat.max(), dp.max(), int((dp > 1e-5).sum()), dp.size))
+    # thresholded modules branch on rounding-level differences: the theta
+    # isosurface iterates while |dp| >= 0.1 hPa, so a particle whose update
+    # lands within ~1e-4 hPa of the threshold stops one iteration earlier or
+    # later (SURVEY App. A: threshold flips are legitimate; measured 2 % of
+    # particles over 50 steps, each off by less than one sub-0.1 hPa update)
+    assert np.mean(dp <= 1e-5) >= 0.95 and dp.max() <= 1e-3
+    assert dlon.max() <= 1e-5 and dlat.max() <= 1e-5
+    np.testing.assert_array_equal(fa.time, ex.time)
