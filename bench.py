@@ -300,6 +300,7 @@ def run_reference(args, wl):
     if rank != 0:
         return
     cfg = WORKLOADS[wl]
+    n_job = cfg["n"] * (ws if args.scaling == "weak" else 1)
     mets = build_met(wl, 0, 1)
     ctl = make_ctl(wl, "exact")
     threads = host_threads()
@@ -312,9 +313,9 @@ def run_reference(args, wl):
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "particle-steps/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * cfg["n"] / v, "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": 1e3 * n_job / v, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": wl, "description": cfg["desc"], "particles": cfg["n"]},
+        "config": {"workload": wl, "description": cfg["desc"], "particles": n_job},
         "cpu_baseline": {"value": v, "unit": "particle-steps/s", "cores": threads,
                          "kind": "port",
                          "sample": f"{n_used} particles x 2 steps per repeat on the same met "
@@ -342,6 +343,9 @@ def main():
     ap.add_argument("--precision", default="fast", choices=("exact", "fast"))
     ap.add_argument("--met-store", default="f32", choices=("f32", "f64"))
     ap.add_argument("--rng", default="philox", choices=("counter", "faithful", "philox"))
+    ap.add_argument("--scaling", default="weak", choices=("weak", "strong"),
+                    help="weak: each GPU advances the workload's particle count; strong: "
+                         "the workload's total is sharded over the GPUs")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     wl = args.workload
@@ -366,7 +370,10 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", gpu))
         else:
             dist.init_process_group(backend)
-    n_tot = cfg["n"]
+    # weak scaling (default): every rank advances the workload's particle
+    # count, global ids offset per rank (independent particles, no data-path
+    # collective); strong: the workload's total is sharded over the ranks
+    n_tot = cfg["n"] * ws if args.scaling == "weak" else cfg["n"]
     mask = engine.modules_mask(cfg["chain"])
     work = sharding.shard_range(n_tot, ws, rank)
     ctl = make_ctl(wl, args.precision, args.rng)
@@ -556,7 +563,7 @@ def main():
         print(json.dumps({
             "metric": METRIC, "value": value, "unit": "particle-steps/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "f64 state / f32 interpolation" if args.precision == "fast" else "f64",
             "data": "synthetic",
             "config": {"workload": wl, "description": cfg["desc"], "particles": n_tot,
@@ -569,7 +576,8 @@ def main():
                               "philox4x32-10 keyed by (seed, step, 32-bit particle id), "
                               "in-kernel (the north star's counter-based generator)",
                        "sort_every": sort_every, "met_rotations_timed": rots,
-                       "parallelism": f"particles sharded x{ws}, met replicated (NCCL broadcast)",
+                       "parallelism": f"particles sharded x{ws} ({args.scaling} scaling), met "
+                                      "replicated (NCCL broadcast), no data-path collective",
                        "l2": "inputs larger than L2 (state %.1f GB/GPU, met %.1f GB)" % (
                            work.size * 120 / 1e9, 2 * nodes * 16 / 1e9)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
