@@ -5,16 +5,18 @@
 
 namespace lt {
 
+// node `which` (0: level k, 1: level k+1) of a record (layout in lt_device.cuh)
 __device__ __forceinline__ void store_node(RecF& r, int which, double u, double v, double w,
                                            double T) {
-  float* d = which ? r.b : r.a;
-  d[0] = static_cast<float>(u); d[1] = static_cast<float>(v);
-  d[2] = static_cast<float>(w); d[3] = static_cast<float>(T);
+  r.x[3 * which] = static_cast<float>(u);
+  r.x[3 * which + 1] = static_cast<float>(v);
+  r.x[3 * which + 2] = static_cast<float>(w);
+  r.x[6 + which] = static_cast<float>(T);
 }
 __device__ __forceinline__ void store_node(RecD& r, int which, double u, double v, double w,
                                            double T) {
-  double* d = which ? r.b.v : r.a.v;
-  d[0] = u; d[1] = v; d[2] = w; d[3] = T;
+  r.x[3 * which] = u; r.x[3 * which + 1] = v; r.x[3 * which + 2] = w;
+  r.x[6 + which] = T;
 }
 
 template <class Src, class Rec>

@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
       // the vertical hop moved only p: the T sample's lon/lat column holds
       const uint32_t r00 = tcol != kNoColumn ? O::cell_in_column(a.met, tcol, p)
                                              : O::cell(a.met, lon, lat, p);
-      gather(a.met.s0, a.met, r00, q);
+      gather(a.met.s0, a.met, r00, q, 7);
       double r = 1.0 - 2.0 * dt / ctl.met_dt;
       r = fmin(fmax(r, 0.0), 1.0);
       const double amp = sqrt(1.0 - r * r);
