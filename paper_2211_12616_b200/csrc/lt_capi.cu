@@ -47,6 +47,8 @@ struct AxisHost {
   int n = 0;
   int logscale = 0;
   float g0 = 0.f, ginv = 0.f;
+  int uniform = 0;
+  double dinv = 0.0;
 };
 
 struct Slot {
@@ -148,6 +150,8 @@ int upload_axis(AxisHost& ax, const double* x, int n, cudaStream_t st) {
   ax.ginv = static_cast<float>((n - 1) / (b - a));
   ax.lo = x[0];
   ax.hi = x[n - 1];
+  ax.uniform = lin <= 1e-9 ? 1 : 0;
+  ax.dinv = (n - 1) / (x[n - 1] - x[0]);
   if (ax.dev && ax.n != n) {
     cudaFree(ax.dev);
     cudaFree(ax.rdx);
@@ -179,6 +183,8 @@ Axis view(const AxisHost& a) {
   v.logscale = a.logscale;
   v.g0 = a.g0;
   v.ginv = a.ginv;
+  v.uniform = a.uniform;
+  v.dinv = a.dinv;
   return v;
 }
 
