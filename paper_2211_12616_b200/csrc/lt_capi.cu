@@ -42,7 +42,7 @@ int fail(int code, const char* fmt, ...) {
 
 struct AxisHost {
   double* dev = nullptr;
-  float* rdx = nullptr;  // fp32 reciprocal cell widths
+  double2* cell = nullptr;  // per cell {x[i], fp32 1/(x[i+1]-x[i]) in the low word}
   double lo = 0.0, hi = 0.0;
   int n = 0;
   int logscale = 0;
@@ -154,21 +154,28 @@ int upload_axis(AxisHost& ax, const double* x, int n, cudaStream_t st) {
   ax.dinv = (n - 1) / (x[n - 1] - x[0]);
   if (ax.dev && ax.n != n) {
     cudaFree(ax.dev);
-    cudaFree(ax.rdx);
+    cudaFree(ax.cell);
     ax.dev = nullptr;
-    ax.rdx = nullptr;
+    ax.cell = nullptr;
   }
   ax.n = n;
   if (!ax.dev) {
     int rc = alloc_dev(reinterpret_cast<void**>(&ax.dev), sizeof(double) * n, "axis");
     if (rc) return rc;
-    rc = alloc_dev(reinterpret_cast<void**>(&ax.rdx), sizeof(float) * n, "axis rdx");
+    rc = alloc_dev(reinterpret_cast<void**>(&ax.cell), sizeof(double2) * n, "axis cells");
     if (rc) return rc;
   }
-  std::vector<float> rdx(n, 0.0f);
-  for (int i = 0; i + 1 < n; ++i) rdx[i] = static_cast<float>(1.0 / (x[i + 1] - x[i]));
+  std::vector<double2> cell(n);
+  for (int i = 0; i < n; ++i) {
+    const float r = i + 1 < n ? static_cast<float>(1.0 / (x[i + 1] - x[i])) : 0.0f;
+    uint32_t bits;
+    std::memcpy(&bits, &r, 4);
+    const uint64_t word = bits;
+    cell[i].x = x[i];
+    std::memcpy(&cell[i].y, &word, 8);
+  }
   CK(cudaMemcpyAsync(ax.dev, x, sizeof(double) * n, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(ax.rdx, rdx.data(), sizeof(float) * n, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(ax.cell, cell.data(), sizeof(double2) * n, cudaMemcpyHostToDevice, st));
   CK(cudaStreamSynchronize(st));
   return LT_OK;
 }
@@ -176,7 +183,7 @@ int upload_axis(AxisHost& ax, const double* x, int n, cudaStream_t st) {
 Axis view(const AxisHost& a) {
   Axis v;
   v.x = a.dev;
-  v.rdx = a.rdx;
+  v.cell = a.cell;
   v.lo = a.lo;
   v.hi = a.hi;
   v.n = a.n;
@@ -349,7 +356,7 @@ int lt_ctx_destroy(lt_ctx* c) {
   free_dev(c->staging);
   for (AxisHost* a : {&c->ax_lon, &c->ax_lat, &c->ax_lev, &c->cl_lat, &c->cl_p}) {
     free_dev(a->dev);
-    free_dev(a->rdx);
+    free_dev(a->cell);
   }
   free_dev(c->hno3);
   free_dev(c->p_trop);
