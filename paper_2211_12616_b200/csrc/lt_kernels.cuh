@@ -8,15 +8,15 @@ namespace lt {
 // node `which` (0: level k, 1: level k+1) of a record (layout in lt_device.cuh)
 __device__ __forceinline__ void store_node(RecF& r, int which, double u, double v, double w,
                                            double T) {
-  r.x[3 * which] = static_cast<float>(u);
-  r.x[3 * which + 1] = static_cast<float>(v);
-  r.x[3 * which + 2] = static_cast<float>(w);
+  r.x[2 * which] = static_cast<float>(u);
+  r.x[2 * which + 1] = static_cast<float>(v);
+  r.x[4 + which] = static_cast<float>(w);
   r.x[6 + which] = static_cast<float>(T);
 }
 __device__ __forceinline__ void store_node(RecD& r, int which, double u, double v, double w,
                                            double T) {
-  r.x[3 * which] = u; r.x[3 * which + 1] = v; r.x[3 * which + 2] = w;
-  r.x[6 + which] = T;
+  r.x[2 * which] = u; r.x[2 * which + 1] = v;
+  r.x[4 + which] = w; r.x[6 + which] = T;
 }
 
 template <class Src, class Rec>

@@ -89,8 +89,13 @@ struct Ops {
     double frev;
     return col * (m.nz - 1) + (m.nz - 2 - locate(m.lev, p, frev));
   }
-  template <class T>
-  __device__ static double spread(const CornersT<T>& q, int f) { return corner_std(q, f); }
+  // corner spreads of u, v, w in met0 around record r00 (meso diffusion)
+  __device__ static void spreads(const MetView<Rec>& m, uint32_t r00, double sig[3]) {
+    Corners<Rec> q;
+    gather(m.s0, m, r00, q, 7);
+#pragma unroll
+    for (int f = 0; f < 3; ++f) sig[f] = corner_std(q, f);
+  }
   // x^e (isosurface potential temperature, physics.py:233-234, 256-257)
   __device__ static double power(double x, double e) { return pow(x, e); }
   __device__ static void normals(uint64_t seed, int64_t step, uint64_t gid, int stream, double z[3]) {
@@ -113,7 +118,11 @@ struct Ops<RecF, true> {
     float frev;
     return col * (m.nz - 1) + (m.nz - 2 - locate_fast(m.lev, p, frev));
   }
-  __device__ static double spread(const CornersT<float>& q, int f) { return corner_std_f(q, f); }
+  __device__ static void spreads(const MetView<RecF>& m, uint32_t r00, double sig[3]) {
+    PairsF q;
+    gather_pairs(m.s0, m, r00, q, 7);
+    corner_std_pairs(q, sig);
+  }
   __device__ static double power(double x, double e) {
     return static_cast<double>(exp2f(static_cast<float>(e) * __log2f(static_cast<float>(x))));
   }
@@ -319,18 +328,18 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
       else
 #endif
       draws<O, RM>(a, s, gid, 2, xm);
-      Corners<Rec> q;
       // the vertical hop moved only p: the T sample's lon/lat column holds
       const uint32_t r00 = tcol != kNoColumn ? O::cell_in_column(a.met, tcol, p)
                                              : O::cell(a.met, lon, lat, p);
-      gather(a.met.s0, a.met, r00, q, 7);
+      double sig[3];
+      O::spreads(a.met, r00, sig);
       double r = 1.0 - 2.0 * dt / ctl.met_dt;
       r = fmin(fmax(r, 0.0), 1.0);
       const double amp = sqrt(1.0 - r * r);
       double pert[3];
 #pragma unroll
       for (int f = 0; f < 3; ++f) {
-        const double sigma = ctl.turb_meso * O::spread(q, f);
+        const double sigma = ctl.turb_meso * sig[f];
         pert[f] = r * ld_state(a.uvwp[f] + src) + amp * sigma * xm[f];
         st_state((PERM ? a.o_uvwp[f] : a.uvwp[f]) + s, pert[f]);
       }
