@@ -776,6 +776,20 @@ static int run_typed(lt_ctx* c, const lt_control* ctl, uint32_t modules, int64_t
   a.iso_nonconv = c->counters;
   static_assert(sizeof(lt_control) == sizeof(Control), "control layout");
   std::memcpy(&a.ctl, ctl, sizeof(Control));
+  {
+    // the kernel's own expressions at dt = dt_model (lt_step.cuh StepConst);
+    // volatile keeps the host compiler from contracting 1 - r*r into an FMA
+    StepConst& k = a.kc;
+    const double dt = ctl->dt_model;
+    k.dt = dt;
+    k.turb_sx = std::sqrt(2.0 * ctl->turb_dx * dt);
+    k.turb_sz = std::sqrt(2.0 * ctl->turb_dz * dt);
+    double r = 1.0 - 2.0 * dt / ctl->met_dt;
+    r = std::fmin(std::fmax(r, 0.0), 1.0);
+    volatile double rr = r * r;
+    k.meso_r = r;
+    k.meso_amp = std::sqrt(1.0 - rr);
+  }
   const bool need_met = modules & (M_ADVECTION | M_TURB | M_MESO | M_SEDI | M_ISOSURF | M_METEO |
                                    M_ISOSURF_INIT);
   if (need_met) {

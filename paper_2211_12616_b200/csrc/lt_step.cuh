@@ -13,6 +13,18 @@
 
 namespace lt {
 
+// Per-launch constants of a full step (dt == ctl.dt_model, the common case):
+// the same fp64 expressions the kernel evaluates per particle, computed once
+// on the host (sqrt and division are correctly rounded on both sides, so a
+// particle taking them gets bit-identical values)
+struct StepConst {
+  double dt;        // ctl.dt_model
+  double turb_sx;   // sqrt(2 turb_dx dt)
+  double turb_sz;   // sqrt(2 turb_dz dt)
+  double meso_r;    // clip(1 - 2 dt / met_dt, 0, 1)
+  double meso_amp;  // sqrt(1 - r^2)
+};
+
 template <class Rec>
 struct StepArgs {
   // particle store (SoA, row stride `cap` for q and uvwp)
@@ -46,6 +58,7 @@ struct StepArgs {
   int64_t faithful_base;
   unsigned long long* iso_nonconv;
   Control ctl;
+  StepConst kc;
   MetView<Rec> met;
   Clim clim;
 };
@@ -81,6 +94,11 @@ struct Ops {
     lt::sample(m, t, lon, lat, p, fmask, out, col);
   }
   __device__ static double over_cos(double x, double lat) { return x / cos_lat(lat); }
+  // physics.py turb vertical hop: p - rho g dz / 100 with rho = 100 p / (R T)
+  __device__ static double vertical_hop(double p, double temp, double dz) {
+    const double rho = 100.0 * p / (kRAir * temp);
+    return p + (-(rho * kG0 * dz) / 100.0);
+  }
   __device__ static uint32_t cell(const MetView<Rec>& m, double lon, double lat, double p) {
     return cell_of(m, lon, lat, p).r00;
   }
@@ -111,6 +129,12 @@ struct Ops<RecF, true> {
     sample_fast(m, t, lon, lat, p, fmask, out, col);
   }
   __device__ static double over_cos(double x, double lat) { return x * inv_cos_lat_fast(lat); }
+  // the same hop as p (1 - g dz / (R T)) with an fp32 reciprocal of T
+  __device__ static double vertical_hop(double p, double temp, double dz) {
+    const double k = static_cast<double>(
+        rcp_approx(static_cast<float>(temp) * static_cast<float>(kRAir / kG0)));
+    return p - p * (dz * k);
+  }
   __device__ static uint32_t cell(const MetView<RecF>& m, double lon, double lat, double p) {
     return cell_fast(m, lon, lat, p).r00;
   }
@@ -306,7 +330,7 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
 #endif
       draws<O, RM>(a, s, gid, 1, xt);
       if (ctl.turb_dx > 0.0) {
-        const double sig = sqrt(2.0 * ctl.turb_dx * dt);
+        const double sig = dt == a.kc.dt ? a.kc.turb_sx : sqrt(2.0 * ctl.turb_dx * dt);
         const double nlon = lon + O::over_cos(sig * xt[0] * kDegPerM, lat);
         lat = lat + sig * xt[1] * kDegPerM;
         lon = nlon;
@@ -314,9 +338,8 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
       if (ctl.turb_dz > 0.0) {
         double v[4];
         O::sample(a.met, time, lon, lat, p, 8, v, &tcol);
-        const double dz = sqrt(2.0 * ctl.turb_dz * dt) * xt[2];
-        const double rho = 100.0 * p / (kRAir * v[3]);
-        p = p + (-(rho * kG0 * dz) / 100.0);
+        const double dz = (dt == a.kc.dt ? a.kc.turb_sz : sqrt(2.0 * ctl.turb_dz * dt)) * xt[2];
+        p = O::vertical_hop(p, v[3], dz);
       }
     }
 
@@ -333,9 +356,12 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
                                              : O::cell(a.met, lon, lat, p);
       double sig[3];
       O::spreads(a.met, r00, sig);
-      double r = 1.0 - 2.0 * dt / ctl.met_dt;
-      r = fmin(fmax(r, 0.0), 1.0);
-      const double amp = sqrt(1.0 - r * r);
+      double r = a.kc.meso_r, amp = a.kc.meso_amp;
+      if (dt != a.kc.dt) {
+        r = 1.0 - 2.0 * dt / ctl.met_dt;
+        r = fmin(fmax(r, 0.0), 1.0);
+        amp = sqrt(1.0 - r * r);
+      }
       double pert[3];
 #pragma unroll
       for (int f = 0; f < 3; ++f) {
