@@ -354,6 +354,11 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
       // the vertical hop moved only p: the T sample's lon/lat column holds
       const uint32_t r00 = tcol != kNoColumn ? O::cell_in_column(a.met, tcol, p)
                                              : O::cell(a.met, lon, lat, p);
+      // the AR(1) state loads go out before the spread gather so the two
+      // latencies overlap
+      double prev[3];
+#pragma unroll
+      for (int f = 0; f < 3; ++f) prev[f] = ld_state(a.uvwp[f] + src);
       double sig[3];
       O::spreads(a.met, r00, sig);
       double r = a.kc.meso_r, amp = a.kc.meso_amp;
@@ -366,7 +371,7 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
 #pragma unroll
       for (int f = 0; f < 3; ++f) {
         const double sigma = ctl.turb_meso * sig[f];
-        pert[f] = r * ld_state(a.uvwp[f] + src) + amp * sigma * xm[f];
+        pert[f] = r * prev[f] + amp * sigma * xm[f];
         st_state((PERM ? a.o_uvwp[f] : a.uvwp[f]) + s, pert[f]);
       }
       const double nlon = lon + O::over_cos(pert[0] * dt * kDegPerM, lat);
