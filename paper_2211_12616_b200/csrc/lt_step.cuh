@@ -94,6 +94,17 @@ struct Ops {
     lt::sample(m, t, lon, lat, p, fmask, out, col);
   }
   __device__ static double over_cos(double x, double lat) { return x / cos_lat(lat); }
+  // one midpoint stage (physics.py:91-116): (xs, ys, zs) <- (lon, lat, p) +
+  // h * wind sampled at (ts, xs, ys, zs)
+  __device__ static void adv_stage(const MetView<Rec>& m, double ts, double& xs, double& ys,
+                                   double& zs, double lon, double lat, double p, double h) {
+    double w[4];
+    sample(m, ts, xs, ys, zs, 7, w);
+    const double nlon = lon + over_cos(w[0] * h * kDegPerM, ys);
+    const double nlat = lat + w[1] * h * kDegPerM;
+    const double np_ = p + w[2] * h;
+    xs = nlon; ys = nlat; zs = np_;
+  }
   // physics.py turb vertical hop: p - rho g dz / 100 with rho = 100 p / (R T)
   __device__ static double vertical_hop(double p, double temp, double dz) {
     const double rho = 100.0 * p / (kRAir * temp);
@@ -129,6 +140,19 @@ struct Ops<RecF, true> {
     sample_fast(m, t, lon, lat, p, fmask, out, col);
   }
   __device__ static double over_cos(double x, double lat) { return x * inv_cos_lat_fast(lat); }
+  // the same stage with fp32 increments (the winds are fp32 already; the
+  // positions they are added to stay fp64)
+  __device__ static void adv_stage(const MetView<RecF>& m, double ts, double& xs, double& ys,
+                                   double& zs, double lon, double lat, double p, double h) {
+    float w[4];
+    sample_fast_f(m, ts, xs, ys, zs, 7, w);
+    const float hf = static_cast<float>(h);
+    const float hk = hf * static_cast<float>(kDegPerM);
+    const float ic = inv_cos_lat_f(ys);
+    xs = lon + static_cast<double>(w[0] * hk * ic);
+    ys = lat + static_cast<double>(w[1] * hk);
+    zs = p + static_cast<double>(w[2] * hf);
+  }
   // the same hop as p (1 - g dz / (R T)) with an fp32 reciprocal of T
   __device__ static double vertical_hop(double p, double temp, double dz) {
     const double k = static_cast<double>(
@@ -302,15 +326,10 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
       double ts = time, xs = lon, ys = lat, zs = p, h = half;
 #pragma unroll 1
       for (int stage = 0; stage < 2; ++stage) {
-        double w[4];
-        O::sample(a.met, ts, xs, ys, zs, 7, w);
         // stage 0: midpoint from (lon, lat, p) with half a step;
         // stage 1: full step from (lon, lat, p) with the midpoint winds
-        const double nlon = lon + O::over_cos(w[0] * h * kDegPerM, ys);
-        const double nlat = lat + w[1] * h * kDegPerM;
-        const double np_ = p + w[2] * h;
+        O::adv_stage(a.met, ts, xs, ys, zs, lon, lat, p, h);
         ts = time + half;
-        xs = nlon; ys = nlat; zs = np_;
         h = dt;
       }
       lon = xs; lat = ys; p = zs;
