@@ -427,7 +427,7 @@ def main():
             stream["rotations"] += 1
             stage_next()
         if sort_every and step % sort_every == 0:
-            eng.sort()
+            eng.sort(mask)
             n_sorts += 1
         if record:
             record[0].record(stream_h)

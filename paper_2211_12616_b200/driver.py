@@ -167,7 +167,7 @@ def run_simulation(ctl, ens, mets, num_devices: int = 1, *, fused: bool = True,
                 def device_step(d, step=step):
                     img = regions[d].image
                     if sort_every and step % sort_every == 0:
-                        img.engine.sort()
+                        img.engine.sort(modules)
                     ctx = img.engine.ctx
                     ctx.timing(True)
                     img.engine.step(img.ctl, step, modules, device_id=d,

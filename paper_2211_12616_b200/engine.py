@@ -206,14 +206,16 @@ class Engine:
                           faithful_state=fstate, chunk=chunk, steps=steps)
         self.sorted = False
 
-    def sort(self) -> None:
+    def sort(self, modules: int | None = None) -> None:
         """Stable box sort of the shard.  Rows the stepping modules do not
         touch (zeta, dt; q unless meteo/decay run; iso_var unless isosurf
         runs) stay in particle order, so the sort moves only the rows the step
         kernel streams — and with all of those cold, the next production-chain
         step applies the permutation itself while it streams them
-        (lt_sort_by_box defers it, lt_run fuses it)."""
-        last = getattr(self, "_last_modules", 0)
+        (lt_sort_by_box defers it, lt_run fuses it).  `modules` is the chain
+        the next steps run (default: the last step's); a row those modules
+        touch kept in particle order would be read and written scattered."""
+        last = modules if modules is not None else getattr(self, "_last_modules", 0)
         home = capi.HOME_ZETA | capi.HOME_DT
         if not (last & (capi.MOD_METEO | capi.MOD_DECAY)):
             home |= capi.HOME_Q      # (a later meteo/decay step still works, via the ids)
