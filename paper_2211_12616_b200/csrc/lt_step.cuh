@@ -23,6 +23,7 @@ struct StepConst {
   double turb_sz;   // sqrt(2 turb_dz dt)
   double meso_r;    // clip(1 - 2 dt / met_dt, 0, 1)
   double meso_amp;  // sqrt(1 - r^2)
+  double decay;     // exp(-dt / decay_tau) (host libm; 1 when decay is off)
 };
 
 template <class Rec>
@@ -105,6 +106,28 @@ struct Ops {
     const double np_ = p + w[2] * h;
     xs = nlon; ys = nlat; zs = np_;
   }
+  // physics.py:206-222 (module_sedi): Stokes settling hop of p
+  __device__ static double sedi_hop(const Control& ctl, double p, double temp, double dt) {
+    const double rho = 100.0 * p / (kRAir * temp);
+    const double vs = 2.0 * (ctl.sedi_radius * ctl.sedi_radius) * (ctl.sedi_density - rho) *
+                      kG0 / (9.0 * kEtaAir);
+    return p + (rho * kG0 * vs * dt) / 100.0;
+  }
+  // physics.py:238-264 (module_isosurf, theta): up to 10 fixed-point steps
+  // p <- 1000 (T(p) / theta0)^(1/kappa) while |dp| >= 0.1; false if still pending
+  __device__ static bool isosurf_theta(const MetView<Rec>& m, double time, double lon, double lat,
+                                       double& p, double theta0) {
+    bool pending = true;
+    for (int it = 0; it < 10 && pending; ++it) {
+      double v[4];
+      sample(m, time, lon, lat, p, 8, v);
+      const double pn = 1000.0 * power(v[3] / theta0, kInvKappa);
+      const double dp = pn - p;
+      p = pn;
+      pending = fabs(dp) >= 0.1;
+    }
+    return !pending;
+  }
   // physics.py turb vertical hop: p - rho g dz / 100 with rho = 100 p / (R T)
   __device__ static double vertical_hop(double p, double temp, double dz) {
     const double rho = 100.0 * p / (kRAir * temp);
@@ -152,6 +175,59 @@ struct Ops<RecF, true> {
     xs = lon + static_cast<double>(w[0] * hk * ic);
     ys = lat + static_cast<double>(w[1] * hk);
     zs = p + static_cast<double>(w[2] * hf);
+  }
+  // the same settling with an fp32 reciprocal of T and no fp64 divisions
+  __device__ static double sedi_hop(const Control& ctl, double p, double temp, double dt) {
+    const double rho = p * (100.0 / kRAir) *
+                       static_cast<double>(rcp_approx(static_cast<float>(temp)));
+    const double vs = (2.0 * kG0 / (9.0 * kEtaAir)) * (ctl.sedi_radius * ctl.sedi_radius) *
+                      (ctl.sedi_density - rho);
+    return p + rho * vs * (dt * (kG0 / 100.0));
+  }
+  // the theta iteration on the column found once (lon/lat do not move
+  // inside it): per step a level lookup, a T-only gather and fp32 pow
+  __device__ static bool isosurf_theta(const MetView<RecF>& m, double time, double lon,
+                                       double lat, double& p, double theta0) {
+    float fx, fy;
+    const int i = locate_fast(m.lon, lon, fx);
+    const int j = locate_fast(m.lat, lat, fy);
+    const uint32_t col = static_cast<uint32_t>(i) * m.ny + j;
+    const float gx = 1.0f - fx, gy = 1.0f - fy;
+    const float xy[4] = {gx * gy, fx * gy, gx * fy, fx * fy};
+    const bool two = m.t1 != m.t0;
+    float wt = two ? static_cast<float>((time - m.t0) * m.inv_dt) : 0.0f;
+    const f32x2 w2 = bc2(fminf(fmaxf(wt, 0.0f), 1.0f));
+    const float inv_theta0 = 1.0f / static_cast<float>(theta0);
+    const uint32_t dcol = m.nz - 1, drow = static_cast<uint32_t>(m.ny) * dcol;
+    bool pending = true;
+#pragma unroll 1
+    for (int it = 0; it < 10 && pending; ++it) {
+      float frev;
+      const int krev = locate_fast(m.lev, p, frev);
+      const uint32_t r00 = col * dcol + (m.nz - 2 - krev);
+      const f32x2 z = pk2(frev, 1.0f - frev);  // (level k, level k+1) weights
+      f32x2 a = pk2(0.0f, 0.0f), b = pk2(0.0f, 0.0f);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint32_t r = r00 + (c & 1 ? drow : 0) + (c & 2 ? dcol : 0);
+        f32x2 t0, t1;
+        asm("ld.global.nc.b64 %0, [%1];" : "=l"(t0) : "l"(m.s0[r].x + 6));
+        const f32x2 wc = mul2(bc2(xy[c]), z);
+        a = fma2(t0, wc, a);
+        if (two) {
+          asm("ld.global.nc.b64 %0, [%1];" : "=l"(t1) : "l"(m.s1[r].x + 6));
+          b = fma2(t1, wc, b);
+        }
+      }
+      if (two) a = fma2(w2, sub2(b, a), a);
+      const float temp = sum2(a);
+      const double pn = static_cast<double>(
+          1000.0f * exp2f(static_cast<float>(kInvKappa) * __log2f(temp * inv_theta0)));
+      const double dp = pn - p;
+      p = pn;
+      pending = fabs(dp) >= 0.1;
+    }
+    return !pending;
   }
   // the same hop as p (1 - g dz / (R T)) with an fp32 reciprocal of T
   __device__ static double vertical_hop(double p, double temp, double dz) {
@@ -411,17 +487,14 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
     if ((mods & M_SEDI) && ctl.sedi_radius != 0.0 && act) {
       double v[4];
       O::sample(a.met, time, lon, lat, p, 8, v);
-      const double rho = 100.0 * p / (kRAir * v[3]);
-      const double vs = 2.0 * (ctl.sedi_radius * ctl.sedi_radius) * (ctl.sedi_density - rho) *
-                        kG0 / (9.0 * kEtaAir);
-      p = p + (rho * kG0 * vs * dt) / 100.0;
+      p = O::sedi_hop(ctl, p, v[3], dt);
     }
 
     // decay (new module): q[slot] *= exp(-dt / tau) while active
     if ((mods & M_DECAY) && ctl.decay_tau > 0.0 && act && ctl.decay_slot >= 0 &&
         ctl.decay_slot < a.nq) {
       double* qs = a.q + static_cast<int64_t>(ctl.decay_slot) * a.cap + row_index(a, s, src, HOME_Q);
-      *qs = *qs * exp(-dt / ctl.decay_tau);
+      *qs = *qs * (dt == a.kc.dt ? a.kc.decay : exp(-dt / ctl.decay_tau));
     }
 
     // physics.py:238-264 (module_isosurf): applies to every particle
@@ -430,16 +503,7 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
         p = a.iso_var[row_index(a, s, src, HOME_ISO)];
       } else {
         const double theta0 = a.iso_var[row_index(a, s, src, HOME_ISO)];
-        bool pending = true;
-        for (int it = 0; it < 10 && pending; ++it) {
-          double v[4];
-          O::sample(a.met, time, lon, lat, p, 8, v);
-          const double pn = 1000.0 * O::power(v[3] / theta0, kInvKappa);
-          const double dp = pn - p;
-          p = pn;
-          pending = fabs(dp) >= 0.1;
-        }
-        nonconv += pending ? 1ull : 0ull;
+        nonconv += O::isosurf_theta(a.met, time, lon, lat, p, theta0) ? 0ull : 1ull;
       }
     }
 
