@@ -299,6 +299,8 @@ int lt_device_count(int32_t* n) {
   return LT_OK;
 }
 
+static int ctx_init(lt_ctx* c);
+
 int lt_ctx_create(int32_t device, lt_ctx** out) {
   *out = nullptr;
   int n = 0;
@@ -307,6 +309,16 @@ int lt_ctx_create(int32_t device, lt_ctx** out) {
   CK(cudaSetDevice(device));
   lt_ctx* c = new lt_ctx();
   c->device = device;
+  if (int rc = ctx_init(c)) {  // release what was created before the failure
+    std::string msg = lt_last_error();
+    lt_ctx_destroy(c);
+    return fail(rc, "%s", msg.c_str());
+  }
+  *out = c;
+  return LT_OK;
+}
+
+static int ctx_init(lt_ctx* c) {
   CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
@@ -322,7 +334,6 @@ int lt_ctx_create(int32_t device, lt_ctx** out) {
   CK(cudaMemsetAsync(c->counters, 0, 8 * sizeof(unsigned long long), c->stream));
   CK(cudaMemsetAsync(c->bad, 0, sizeof(int), c->stream));
   CK(cudaStreamSynchronize(c->stream));
-  *out = c;
   return LT_OK;
 }
 
