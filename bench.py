@@ -452,7 +452,10 @@ def main():
             ev[1].record(stream_h)
             barrier()
         total = ev[0].elapsed_time(ev[1])
-        kern = statistics.mean(ev[2 + 2 * k].elapsed_time(ev[3 + 2 * k]) for k in range(k_steps))
+        per = [ev[2 + 2 * k].elapsed_time(ev[3 + 2 * k]) for k in range(k_steps)]
+        kern = statistics.mean(per)
+        if os.environ.get("LT_BENCH_PER_STEP"):
+            print("per-step kernel ms:", " ".join(f"{t:.3f}" for t in per), file=sys.stderr)
         total, kern = sharding.max_over_ranks([total, kern], dist, "cuda")
         return total, kern, clk.summary(), n_sorts - sorts0, \
             (stream["rotations"] - rot0 if stream else 0)
