@@ -333,6 +333,13 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
       }
       if (a.ids && (mods & (M_TURB | M_MESO | M_CONVECTION))) prefetch_l2(a.ids + nx);
     }
+    if (PERM && s + stride < s_hi) {  // the next tile's gathered source rows
+      const int64_t nx = a.perm_start + a.perm[s + stride - a.perm_start];
+      prefetch_l2(a.time + nx); prefetch_l2(a.lon + nx); prefetch_l2(a.lat + nx);
+      prefetch_l2(a.p + nx);
+      prefetch_l2(a.uvwp[0] + nx); prefetch_l2(a.uvwp[1] + nx); prefetch_l2(a.uvwp[2] + nx);
+      prefetch_l2(a.ids + nx);
+    }
 #endif
     double time = ld_state(a.time + src), lon = ld_state(a.lon + src), lat = ld_state(a.lat + src),
            p = ld_state(a.p + src);
