@@ -431,3 +431,40 @@ def test_fast_full_chain_within_tolerance(eng, golden_chain):
     assert np.mean(dp <= 1e-5) >= 0.95 and dp.max() <= 1e-3
     assert dlon.max() <= 1e-5 and dlat.max() <= 1e-5
     np.testing.assert_array_equal(fa.time, ex.time)
+
+
+@pytest.mark.parametrize("same_time", [False, True])
+def test_fast_path_regional_irregular_grid(eng, same_time):
+    """The fast path's own cell logic — computed cells on uniform axes, fp32
+    fraction search on irregular ones, the clamp folded into index and
+    fraction — against the exact kernels on a regional (non-periodic) grid
+    with irregular latitudes, particles partly outside the hull, and the
+    single-snapshot (t0 == t1) case."""
+    engine, ms, _ = eng
+    rs = np.random.default_rng(7)
+    f32 = lambda x: np.asarray(x, dtype=np.float32).astype(np.float64)
+    lons = f32(np.arange(0.0, 91.0, 3.0))                                  # uniform
+    lats = f32(np.sort(np.r_[-60.0, 60.0, rs.uniform(-59.0, 59.0, 29)]))   # irregular
+    levs = f32(np.geomspace(1000.0, 50.0, 12))
+    shape = (lons.size, lats.size, levs.size)
+    lo3, la3 = np.meshgrid(lons, lats, indexing="ij")
+    base = lambda a, b: f32((a + b * np.cos(np.deg2rad(la3)) * np.sin(np.deg2rad(3 * lo3)))[..., None]
+                            * np.ones(shape))
+    def snap(t, ph):
+        return ms.MeteoField(t, lons, lats, levs, base(10.0 + ph, 5.0), base(2.0, 3.0 + ph),
+                             f32(1e-3 * np.ones(shape)), base(250.0 + ph, 10.0))
+    m0 = snap(0.0, 0.0)
+    m1 = m0 if same_time else snap(3600.0, 1.0)
+    n = 20000
+    ens = ms.ParticleEnsemble(np=n, time=np.zeros(n), p=rs.uniform(30.0, 1100.0, n),
+                              zeta=np.zeros(n), lon=rs.uniform(-20.0, 110.0, n),
+                              lat=rs.uniform(-70.0, 70.0, n), q=np.zeros((5, n)))
+    kw = dict(t_stop=1800.0, dt_model=180.0, met_dt=3600.0, rng_mode="counter", rng_seed_global=3)
+    exact = _engine_run(engine, m0, m1, ens, ms.Control(**kw), 10, engine.ADV_DIFF, 5)
+    fast = _engine_run(engine, m0, m1, ens, ms.Control(precision="fast", **kw), 10,
+                       engine.ADV_DIFF, 5)
+    dlon = np.abs((fast.lon - exact.lon + 180.0) % 360.0 - 180.0)
+    assert dlon.max() / 360.0 <= 1e-5
+    assert np.abs(fast.lat - exact.lat).max() / 180.0 <= 1e-5
+    assert (np.abs(fast.p - exact.p) / exact.p).max() <= 1e-5
+    np.testing.assert_array_equal(fast.time, exact.time)
