@@ -347,8 +347,8 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
     // physics.py:82-88 (module_timesteps)
     double dt;
     if ((mods & M_TIMESTEPS) || !(a.flags & F_DT_ARRAY)) {
-      dt = fmin(ctl.dt_model, ctl.t_stop - time);
-      dt = fmin(fmax(dt, 0.0), ctl.dt_model);
+      dt = np_min(ctl.t_stop - time, ctl.dt_model);
+      dt = np_min(np_max(dt, 0.0), ctl.dt_model);
       if ((mods & M_TIMESTEPS) && (a.flags & F_WRITE_DT)) a.dt[row_index(a, s, src, HOME_DT)] = dt;
     } else {
       dt = a.dt[row_index(a, s, src, HOME_DT)];
@@ -466,7 +466,7 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
       double r = a.kc.meso_r, amp = a.kc.meso_amp;
       if (dt != a.kc.dt) {
         r = 1.0 - 2.0 * dt / ctl.met_dt;
-        r = fmin(fmax(r, 0.0), 1.0);
+        r = np_min(np_max(r, 0.0), 1.0);
         amp = sqrt(1.0 - r * r);
       }
       double pert[3];
@@ -529,7 +529,7 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
         }
         lon = m - 180.0;
       }
-      p = fmin(fmax(p, ctl.p_top), ctl.p_surf);
+      p = np_min(np_max(p, ctl.p_top), ctl.p_surf);
     }
 
     // physics.py:290-301 (module_meteo): sample T,u,v and climatology
