@@ -12,7 +12,7 @@ constexpr uint32_t kChainAdvDiff = M_TIMESTEPS | M_ADVECTION | M_TURB | M_MESO |
 constexpr uint32_t kChainPlume = kChainAdvDiff | M_SEDI | M_DECAY;
 constexpr uint32_t kChainFull = kChainAdvDiff | M_CONVECTION | M_SEDI | M_DECAY | M_ISOSURF | M_METEO;
 
-template <class Rec, uint32_t FIXED, bool FAST, int RM, bool PERM = false>
+template <class Rec, uint32_t FIXED, int FAST, int RM, bool PERM = false>
 static cudaError_t launch_fixed(const StepArgs<Rec>& a, cudaStream_t st) {
   static int blocks_per_sm = 0;
   static int sms = 0;
@@ -35,7 +35,7 @@ static cudaError_t launch_fixed(const StepArgs<Rec>& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-template <class Rec, bool FAST>
+template <class Rec, int FAST>
 static cudaError_t launch_prec(const StepArgs<Rec>& a, cudaStream_t st) {
   // the production chain gets its in-kernel generator fixed at compile time;
   // with a pending box-sort permutation it applies it on the fly
@@ -75,9 +75,17 @@ bool perm_capable(uint32_t modules, uint32_t flags, int rng_mode) {
 
 template <class Rec>
 cudaError_t launch_step(const StepArgs<Rec>& a, cudaStream_t st) {
-  // the fast (mixed-precision) kernels exist for the fp32 met store only
-  if (a.ctl.precision == 1 && sizeof(Rec) == sizeof(RecF)) return launch_prec<Rec, true>(a, st);
-  return launch_prec<Rec, false>(a, st);
+  // the fast (mixed-precision) kernels exist for the fp32 met store only;
+  // a geographic grid (uniform lon/lat, levels with the log2 guess) gets
+  // its axis lookups fixed at compile time
+  if constexpr (sizeof(Rec) == sizeof(RecF)) {
+    if (a.ctl.precision == 1) {
+      const bool geo = a.met.lon.uniform && a.met.lat.uniform && !a.met.lev.uniform &&
+                       a.met.lev.logscale;
+      return geo ? launch_prec<Rec, 2>(a, st) : launch_prec<Rec, 1>(a, st);
+    }
+  }
+  return launch_prec<Rec, 0>(a, st);
 }
 template cudaError_t launch_step<RecF>(const StepArgs<RecF>&, cudaStream_t);
 template cudaError_t launch_step<RecD>(const StepArgs<RecD>&, cudaStream_t);

@@ -85,9 +85,10 @@ __device__ __forceinline__ void st_state(double* p, double v) { *p = v; }
 #define LT_STEP_MIN_BLOCKS (1024 / LT_STEP_BLOCK)
 #endif
 
-// Arithmetic policy: EXACT reproduces numpy's operation sequence in fp64;
-// FAST is the mixed-precision path of lt_device.cuh (fp32 store only).
-template <class Rec, bool FAST>
+// Arithmetic policy: FAST = 0 reproduces numpy's operation sequence in
+// fp64; FAST = 1 is the mixed-precision path of lt_device.cuh (fp32 store
+// only), FAST = 2 the same on a geographic grid (locate_h / locate_v).
+template <class Rec, int FAST>
 struct Ops {
   static constexpr bool kFast = false;
   __device__ static void sample(const MetView<Rec>& m, double t, double lon, double lat,
@@ -155,12 +156,12 @@ struct Ops {
   }
 };
 
-template <>
-struct Ops<RecF, true> {
+template <int G>
+struct OpsFast {
   static constexpr bool kFast = true;
   __device__ static void sample(const MetView<RecF>& m, double t, double lon, double lat,
                                 double p, int fmask, double out[4], uint32_t* col = nullptr) {
-    sample_fast(m, t, lon, lat, p, fmask, out, col);
+    sample_fast<G>(m, t, lon, lat, p, fmask, out, col);
   }
   __device__ static double over_cos(double x, double lat) { return x * inv_cos_lat_fast(lat); }
   // the same stage with fp32 increments (the winds are fp32 already; the
@@ -168,7 +169,7 @@ struct Ops<RecF, true> {
   __device__ static void adv_stage(const MetView<RecF>& m, double ts, double& xs, double& ys,
                                    double& zs, double lon, double lat, double p, double h) {
     float w[4];
-    sample_fast_f(m, ts, xs, ys, zs, 7, w);
+    sample_fast_f<G>(m, ts, xs, ys, zs, 7, w);
     const float hf = static_cast<float>(h);
     const float hk = hf * static_cast<float>(kDegPerM);
     const float ic = inv_cos_lat_f(ys);
@@ -189,8 +190,8 @@ struct Ops<RecF, true> {
   __device__ static bool isosurf_theta(const MetView<RecF>& m, double time, double lon,
                                        double lat, double& p, double theta0) {
     float fx, fy;
-    const int i = locate_fast(m.lon, lon, fx);
-    const int j = locate_fast(m.lat, lat, fy);
+    const int i = locate_h<G>(m.lon, lon, fx);
+    const int j = locate_h<G>(m.lat, lat, fy);
     const uint32_t col = static_cast<uint32_t>(i) * m.ny + j;
     const float gx = 1.0f - fx, gy = 1.0f - fy;
     const float xy[4] = {gx * gy, fx * gy, gx * fy, fx * fy};
@@ -203,7 +204,7 @@ struct Ops<RecF, true> {
 #pragma unroll 1
     for (int it = 0; it < 10 && pending; ++it) {
       float frev;
-      const int krev = locate_fast(m.lev, p, frev);
+      const int krev = locate_v<G>(m.lev, p, frev);
       const uint32_t r00 = col * dcol + (m.nz - 2 - krev);
       const f32x2 z = pk2(frev, 1.0f - frev);  // (level k, level k+1) weights
       f32x2 a = pk2(0.0f, 0.0f), b = pk2(0.0f, 0.0f);
@@ -236,11 +237,11 @@ struct Ops<RecF, true> {
     return p - p * (dz * k);
   }
   __device__ static uint32_t cell(const MetView<RecF>& m, double lon, double lat, double p) {
-    return cell_fast(m, lon, lat, p).r00;
+    return cell_fast<G>(m, lon, lat, p).r00;
   }
   __device__ static uint32_t cell_in_column(const MetView<RecF>& m, uint32_t col, double p) {
     float frev;
-    return col * (m.nz - 1) + (m.nz - 2 - locate_fast(m.lev, p, frev));
+    return col * (m.nz - 1) + (m.nz - 2 - locate_v<G>(m.lev, p, frev));
   }
   __device__ static void spreads(const MetView<RecF>& m, uint32_t r00, double sig[3]) {
     PairsF q;
@@ -254,6 +255,8 @@ struct Ops<RecF, true> {
     counter_normals_fast(seed, step, gid, stream, z);
   }
 };
+template <> struct Ops<RecF, 1> : OpsFast<1> {};
+template <> struct Ops<RecF, 2> : OpsFast<2> {};
 
 // Draws of one stream for particle slot s / global id gid: stream 0 = the
 // convection uniform (x[0]), 1 = turbulent normals, 2 = mesoscale normals.
@@ -303,7 +306,7 @@ __device__ __forceinline__ int64_t row_index(const StepArgs<Rec>& a, int64_t s, 
   return (a.home_mask & group) && a.ids ? static_cast<int64_t>(a.ids[src]) - a.home_base : s;
 }
 
-template <class Rec, uint32_t FIXED, bool FAST, int RM, bool PERM>
+template <class Rec, uint32_t FIXED, int FAST, int RM, bool PERM>
 __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel(const StepArgs<Rec> a) {
   using O = Ops<Rec, FAST>;
   const uint32_t mods = FIXED ? FIXED : a.modules;
@@ -370,7 +373,7 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
     // issue slots the gathers leave idle
     // (the exact path measured slower this way: its fp64 normals cost twice
     // the registers)
-    constexpr bool kEarly = FAST && RM >= 0;
+    constexpr bool kEarly = FAST != 0 && RM >= 0;
     float early[6];
     if (kEarly && act) {
       if (RM == RNG_FAITHFUL) {
