@@ -320,6 +320,12 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
   const int64_t stride = blockDim.x;
   unsigned long long nonconv = 0;
 
+  // per-launch switches, decided once outside the particle loop
+  const bool want_turb = (mods & M_TURB) && (ctl.turb_dx != 0.0 || ctl.turb_dz != 0.0);
+  const bool want_meso = (mods & M_MESO) && ctl.turb_meso != 0.0;
+  const bool want_conv = (mods & M_CONVECTION) && ctl.conv_prob != 0.0;
+  const bool turb_h = ctl.turb_dx > 0.0, turb_v = ctl.turb_dz > 0.0;
+
   for (int64_t s = s_lo + threadIdx.x; s < s_hi; s += stride) {
     // PERM: this slot's particle comes from old slot `src` (box sort applied
     // on the fly: gathered reads, coalesced writes to the o_* rows)
@@ -361,9 +367,6 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
     // random draws (rng.py:156-181) are made where they are consumed, which
     // keeps them out of the registers live across the advection gathers —
     // except on the fast counter path, below
-    const bool want_turb = (mods & M_TURB) && (ctl.turb_dx != 0.0 || ctl.turb_dz != 0.0);
-    const bool want_meso = (mods & M_MESO) && ctl.turb_meso != 0.0;
-    const bool want_conv = (mods & M_CONVECTION) && ctl.conv_prob != 0.0;
     const uint64_t gid = (RM >= 0 || (a.flags & F_RNG_INKERNEL)) && (want_turb || want_meso || want_conv)
                              ? (a.ids ? static_cast<uint64_t>(a.ids[src]) : static_cast<uint64_t>(s))
                              : 0ull;
@@ -434,13 +437,13 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
       else
 #endif
       draws<O, RM>(a, s, gid, 1, xt);
-      if (ctl.turb_dx > 0.0) {
+      if (turb_h) {
         const double sig = dt == a.kc.dt ? a.kc.turb_sx : sqrt(2.0 * ctl.turb_dx * dt);
         const double nlon = lon + O::over_cos(sig * xt[0] * kDegPerM, lat);
         lat = lat + sig * xt[1] * kDegPerM;
         lon = nlon;
       }
-      if (ctl.turb_dz > 0.0) {
+      if (turb_v) {
         double v[4];
         O::sample(a.met, time, lon, lat, p, 8, v, &tcol);
         const double dz = (dt == a.kc.dt ? a.kc.turb_sz : sqrt(2.0 * ctl.turb_dz * dt)) * xt[2];
