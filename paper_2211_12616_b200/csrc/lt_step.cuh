@@ -438,7 +438,8 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
 #endif
       draws<O, RM>(a, s, gid, 1, xt);
       if (turb_h) {
-        const double sig = dt == a.kc.dt ? a.kc.turb_sx : sqrt(2.0 * ctl.turb_dx * dt);
+        double sig = a.kc.turb_sx;
+        if (__builtin_expect(dt != a.kc.dt, 0)) sig = sqrt(2.0 * ctl.turb_dx * dt);
         const double nlon = lon + O::over_cos(sig * xt[0] * kDegPerM, lat);
         lat = lat + sig * xt[1] * kDegPerM;
         lon = nlon;
@@ -446,7 +447,9 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
       if (turb_v) {
         double v[4];
         O::sample(a.met, time, lon, lat, p, 8, v, &tcol);
-        const double dz = (dt == a.kc.dt ? a.kc.turb_sz : sqrt(2.0 * ctl.turb_dz * dt)) * xt[2];
+        double sz = a.kc.turb_sz;
+        if (__builtin_expect(dt != a.kc.dt, 0)) sz = sqrt(2.0 * ctl.turb_dz * dt);
+        const double dz = sz * xt[2];
         p = O::vertical_hop(p, v[3], dz);
       }
     }
@@ -470,7 +473,7 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
       double sig[3];
       O::spreads(a.met, r00, sig);
       double r = a.kc.meso_r, amp = a.kc.meso_amp;
-      if (dt != a.kc.dt) {
+      if (__builtin_expect(dt != a.kc.dt, 0)) {
         r = 1.0 - 2.0 * dt / ctl.met_dt;
         r = np_min(np_max(r, 0.0), 1.0);
         amp = sqrt(1.0 - r * r);
