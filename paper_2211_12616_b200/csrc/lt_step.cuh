@@ -24,6 +24,7 @@ struct StepConst {
   double meso_r;    // clip(1 - 2 dt / met_dt, 0, 1)
   double meso_amp;  // sqrt(1 - r^2)
   double decay;     // exp(-dt / decay_tau) (host libm; 1 when decay is off)
+  double conv_scale;  // (p_surf - conv_p_top) / conv_prob (fast path only)
 };
 
 template <class Rec>
@@ -107,6 +108,10 @@ struct Ops {
     const double np_ = p + w[2] * h;
     xs = nlon; ys = nlat; zs = np_;
   }
+  // physics.py:199-203: the convective target level of a uniform u < conv_prob
+  __device__ static double conv_target(const Control& ctl, const StepConst&, double u) {
+    return ctl.conv_p_top + (u / ctl.conv_prob) * (ctl.p_surf - ctl.conv_p_top);
+  }
   // physics.py:206-222 (module_sedi): Stokes settling hop of p
   __device__ static double sedi_hop(const Control& ctl, double p, double temp, double dt) {
     const double rho = 100.0 * p / (kRAir * temp);
@@ -177,6 +182,9 @@ struct OpsFast {
     ys = lat + static_cast<double>(w[1] * hk);
     zs = p + static_cast<double>(w[2] * hf);
   }
+  __device__ static double conv_target(const Control& ctl, const StepConst& kc, double u) {
+    return ctl.conv_p_top + u * kc.conv_scale;
+  }
   // the same settling with an fp32 reciprocal of T and no fp64 divisions
   __device__ static double sedi_hop(const Control& ctl, double p, double temp, double dt) {
     const double rho = p * (100.0 / kRAir) *
@@ -198,7 +206,7 @@ struct OpsFast {
     const bool two = m.t1 != m.t0;
     float wt = two ? static_cast<float>((time - m.t0) * m.inv_dt) : 0.0f;
     const f32x2 w2 = bc2(fminf(fmaxf(wt, 0.0f), 1.0f));
-    const float inv_theta0 = 1.0f / static_cast<float>(theta0);
+    const float inv_theta0 = rcp_approx(static_cast<float>(theta0));
     const uint32_t dcol = m.nz - 1, drow = static_cast<uint32_t>(m.ny) * dcol;
     bool pending = true;
 #pragma unroll 1
@@ -223,7 +231,7 @@ struct OpsFast {
       if (two) a = fma2(w2, sub2(b, a), a);
       const float temp = sum2(a);
       const double pn = static_cast<double>(
-          1000.0f * exp2f(static_cast<float>(kInvKappa) * __log2f(temp * inv_theta0)));
+          1000.0f * ex2_approx(static_cast<float>(kInvKappa) * __log2f(temp * inv_theta0)));
       const double dp = pn - p;
       p = pn;
       pending = fabs(dp) >= 0.1;
@@ -249,7 +257,7 @@ struct OpsFast {
     corner_std_pairs(q, sig);
   }
   __device__ static double power(double x, double e) {
-    return static_cast<double>(exp2f(static_cast<float>(e) * __log2f(static_cast<float>(x))));
+    return static_cast<double>(ex2_approx(static_cast<float>(e) * __log2f(static_cast<float>(x))));
   }
   __device__ static void normals(uint64_t seed, int64_t step, uint64_t gid, int stream, double z[3]) {
     counter_normals_fast(seed, step, gid, stream, z);
@@ -496,7 +504,7 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
       double xc[3];
       draws<O, RM>(a, s, gid, 0, xc);
       if (p > ctl.conv_p_top && xc[0] < ctl.conv_prob)
-        p = ctl.conv_p_top + (xc[0] / ctl.conv_prob) * (ctl.p_surf - ctl.conv_p_top);
+        p = O::conv_target(ctl, a.kc, xc[0]);
     }
 
     // physics.py:206-222 (module_sedi): Stokes settling
