@@ -367,18 +367,23 @@ def part1by1(x):
     return x
 
 
+BOX_LEVELS = 2   # level cells per sort box (lt_kernels.cuh LT_BOX_ZDIV)
+
+
 def box_keys(snap: Snapshot, lon, lat, p):
     """Sort key of the met cell (i, j, k) of each particle (new north-star
     component; the cell is pinned through the reference locate): the lon/lat
-    column in Z (Morton) order, bits of i above those of j, times (nz-1),
-    plus the level cell k — when that fits 32 bits, else the linear record
-    index ((i*ny)+j)*(nz-1)+k.  Mirrors lt_sort_by_box."""
+    column in Z (Morton) order, bits of i above those of j, times the number
+    of level boxes, plus the level box k // BOX_LEVELS — when that fits 32
+    bits, else the linear record index ((i*ny)+j)*(nz-1)+k.  Mirrors
+    lt_sort_by_box."""
     i, j, k, _, _, _ = cell_of(snap, lon, lat, p)
     nx, ny, nz = snap.lons.shape[0], snap.lats.shape[0], snap.levs.shape[0]
-    top = int((part1by1(nx - 1) << np.uint64(1)) | part1by1(ny - 1)) * (nz - 1) + (nz - 2)
+    nb = (nz - 2) // BOX_LEVELS + 1
+    top = int((part1by1(nx - 1) << np.uint64(1)) | part1by1(ny - 1)) * nb + (nb - 1)
     if nx <= 65536 and ny <= 65536 and top < 2 ** 32:
         col = (part1by1(i) << np.uint64(1)) | part1by1(j)
-        return (col * np.uint64(nz - 1) + k.astype(np.uint64)).astype(np.int64)
+        return (col * np.uint64(nb) + (k // BOX_LEVELS).astype(np.uint64)).astype(np.int64)
     return ((i.astype(np.int64) * ny + j) * (nz - 1) + k).astype(np.int64)
 
 

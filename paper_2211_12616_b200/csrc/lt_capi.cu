@@ -1059,8 +1059,9 @@ static int sort_typed(lt_ctx* c, int64_t start, int64_t end) {
   // grids; measured -1.6 % step time against row-major cells at cfg3), else
   // the record index
   const uint64_t max_morton =
-      static_cast<uint64_t>((part1by1(static_cast<uint32_t>(c->nx - 1)) << 1) |
-                            part1by1(static_cast<uint32_t>(c->ny - 1))) * (c->nz - 1) + (c->nz - 2);
+      static_cast<uint64_t>((part1by1(static_cast<uint32_t>(c->nx - 1) >> LT_BOX_SHIFT) << 1) |
+                            part1by1(static_cast<uint32_t>(c->ny - 1) >> LT_BOX_SHIFT)) *
+          box_levels(c->nz) + (box_levels(c->nz) - 1);
   const int morton = c->nx <= 65536 && c->ny <= 65536 && max_morton < (uint64_t(1) << 32);
   CK(launch_box_keys<Rec>(m, c->lon, c->lat, c->p, start, n, keys_in, vals_in, morton, c->stream));
   const uint64_t max_key = morton ? max_morton : static_cast<uint64_t>(n_rec(c));

@@ -100,9 +100,11 @@ def test_met_periodic_rule():
     np.testing.assert_array_equal(ref.lons, closed.lons)
 
 
-def test_box_keys_are_a_bijection_of_cells():
-    """The sort key (Morton lon/lat column, level fastest) is injective over
-    cells and orders columns in Z order, levels ascending inside a column."""
+def test_box_keys_order_columns_then_level_pairs():
+    """The sort key (Morton lon/lat column, then the pair of level cells k//2
+    — two consecutive 32-byte records) is injective over such boxes, equal
+    inside one, and orders columns in Z order, level boxes ascending inside a
+    column."""
     from paper_2211_12616_b200 import synthetic
     lons, lats, levs = synthetic.grid(30.0, 20.0, 6)
     f = synthetic.era5_like(lons, lats, levs)
@@ -116,10 +118,13 @@ def test_box_keys_are_a_bijection_of_cells():
     rev = snap.levs[::-1]
     p = (rev[kk] + rev[kk + 1]) / 2
     keys = orc.box_keys(snap, lon.ravel(), lat.ravel(), p.ravel())
-    assert np.unique(keys).size == keys.size
-
-    def morton(i, j):
-        return sum(((i >> b) & 1) << (2 * b + 1) | ((j >> b) & 1) << (2 * b) for b in range(16))
     i, j, k, *_ = orc.cell_of(snap, lon.ravel(), lat.ravel(), p.ravel())
-    brute = np.array([morton(int(a), int(b)) * (nz - 1) + int(c) for a, b, c in zip(i, j, k)])
+    boxes = np.stack([i, j, k // orc.BOX_LEVELS], axis=1)
+    assert np.unique(keys).size == np.unique(boxes, axis=0).shape[0]
+
+    def morton(a, b):
+        return sum(((a >> t) & 1) << (2 * t + 1) | ((b >> t) & 1) << (2 * t) for t in range(16))
+    nb = (nz - 2) // orc.BOX_LEVELS + 1
+    brute = np.array([morton(int(a), int(b)) * nb + int(c) // orc.BOX_LEVELS
+                      for a, b, c in zip(i, j, k)])
     np.testing.assert_array_equal(keys, brute)
