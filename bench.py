@@ -484,6 +484,44 @@ def main():
         if args.rng != "counter":
             alt_rng = alt_run(args.precision, "counter", k_other)
 
+    # the same steps with the sort cadence, but every run of steps between
+    # two sorts is one multi-step launch (Engine.step_many: each particle
+    # advanced in registers; identical results) — informational beside the
+    # one-launch-per-step headline
+    multi = None
+    if k_other > 0 and stream is None and args.rng in ("counter", "philox") and \
+            not any(m in cfg["chain"] for m in ("meteo", "decay")):
+        nonlocal_step = [step]
+
+        def run_multi(k_steps):
+            ev0, ev1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
+            st = nonlocal_step[0]
+            with ClockSampler(gpu) as clk:
+                ev0.record(stream_h)
+                done = 0
+                while done < k_steps:
+                    if sort_every and st % sort_every == 0:
+                        eng.sort(mask)
+                    run = k_steps - done
+                    if sort_every:
+                        run = min(run, sort_every - st % sort_every)
+                    eng.step_many(ctl, st, run, mask)
+                    st += run
+                    done += run
+                ev1.record(stream_h)
+                barrier()
+            nonlocal_step[0] = st
+            t = sharding.max_over_ranks([ev0.elapsed_time(ev1)], dist, "cuda")[0]
+            return t, clk.summary()
+
+        run_multi(min(k_other, 15))            # warm-up of the multi-step kernels
+        t_m, clk_m = run_multi(k_other)
+        step = nonlocal_step[0]
+        multi = {"value": n_tot * k_other / (t_m / 1e3), "ms_per_step": t_m / k_other,
+                 "steps": k_other, "sort_every": sort_every, "clocks": clk_m,
+                 "launches": "one per run of steps between sorts (the first step after a "
+                             "sort applies its permutation alone)"}
+
     # e2e: the public host-buffer API (Engine.step_host -> lt_run_host): the
     # shard's SoA sits in pinned host memory; every step streams it through
     # the GPU (H2D, fused step, D2H overlapped in chunks) and lands back.
@@ -589,7 +627,7 @@ def main():
                          "algorithmic_bytes_per_particle_step": b, "issue": issue,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks
                          else "fallback"},
-            "alt_precision": other, "alt_rng": alt_rng,
+            "alt_precision": other, "alt_rng": alt_rng, "alt_multistep": multi,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": launches,
         }), flush=True)

@@ -162,6 +162,14 @@ int lt_clim_load(lt_ctx *ctx, int32_t nlat, int32_t np_, const double *lat_grid,
 int lt_run(lt_ctx *ctx, const lt_control *ctl, uint32_t modules, int64_t start,
            int64_t end, int64_t step, uint64_t faithful_state,
            int64_t faithful_base, uint32_t flags);
+/* nsteps consecutive steps; results identical to nsteps lt_run calls.  The
+   production chain (timesteps|advection|turb|meso|position) with in-kernel
+   counter or philox draws runs as one launch, each particle's state held in
+   registers across the steps (a pending box-sort permutation is applied by
+   a first single step); anything else as nsteps launches.  The selected met
+   pair must cover all the steps. */
+int lt_run_steps(lt_ctx *ctx, const lt_control *ctl, uint32_t modules, int64_t start,
+                 int64_t end, int64_t step, int32_t nsteps, uint32_t flags);
 /* host-buffer step (the module API's numpy path, physics.py:82-301 called
    on host arrays): particles [0, n) live in host memory (pinned for full
    PCIe overlap).  They stream through the context's particle store in

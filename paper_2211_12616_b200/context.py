@@ -243,6 +243,13 @@ class DeviceContext:
         capi.check(self.lib.lt_run(self.h, C.byref(c), modules, start, end, step,
                                    faithful_state & 0xFFFFFFFFFFFFFFFF, faithful_base, flags))
 
+    def run_steps(self, ctl, modules: int, start: int, end: int, step: int, nsteps: int,
+                  flags: int = 0) -> None:
+        """lt_run_steps: `nsteps` consecutive steps in one launch."""
+        c = ctl if isinstance(ctl, capi.LtControl) else capi.control_struct(ctl)
+        capi.check(self.lib.lt_run_steps(self.h, C.byref(c), modules, start, end, step,
+                                          int(nsteps), flags))
+
     def run_host(self, ctl, modules: int, n: int, step: int, first_id: int, time, p, lon, lat,
                  uvwp=None, iso_var=None, q=None, faithful_state: int = 0,
                  chunk: int = 0, steps: int = 1) -> None:

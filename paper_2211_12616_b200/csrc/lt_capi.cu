@@ -756,7 +756,7 @@ extern "C++" {
 template <class Rec>
 static int run_typed(lt_ctx* c, const lt_control* ctl, uint32_t modules, int64_t start,
                      int64_t end, int64_t step, uint64_t fstate, int64_t fbase, uint32_t flags,
-                     bool fuse_perm = false) {
+                     bool fuse_perm = false, int32_t nsteps = 1) {
   StepArgs<Rec> a;
   a.perm = nullptr;
   a.perm_start = 0;
@@ -782,7 +782,7 @@ static int run_typed(lt_ctx* c, const lt_control* ctl, uint32_t modules, int64_t
   a.home_base = c->home_base;
   a.rnd_conv = c->rnd_conv; a.rnd_turb = c->rnd_turb; a.rnd_meso = c->rnd_meso;
   a.cap = c->cap; a.start = start; a.end = end; a.nq = c->nq;
-  a.modules = modules; a.flags = flags; a.step = step;
+  a.modules = modules; a.flags = flags; a.step = step; a.nsteps = nsteps;
   a.faithful_state = fstate; a.faithful_base = fbase;
   a.iso_nonconv = c->counters;
   static_assert(sizeof(lt_control) == sizeof(Control), "control layout");
@@ -832,8 +832,47 @@ static int run_typed(lt_ctx* c, const lt_control* ctl, uint32_t modules, int64_t
 }
 }  // extern C++
 
+static int run_impl(lt_ctx* c, const lt_control* ctl, uint32_t modules, int64_t start,
+                    int64_t end, int64_t step, int32_t nsteps, uint64_t fstate, int64_t fbase,
+                    uint32_t flags);
+
 int lt_run(lt_ctx* c, const lt_control* ctl, uint32_t modules, int64_t start, int64_t end,
            int64_t step, uint64_t fstate, int64_t fbase, uint32_t flags) {
+  return run_impl(c, ctl, modules, start, end, step, 1, fstate, fbase, flags);
+}
+
+// nsteps consecutive steps of [start, end) in one launch (each particle's
+// state stays in registers across them): in-kernel counter or Philox draws
+// only, and the met pair must cover all the steps (no rotation inside)
+int lt_run_steps(lt_ctx* c, const lt_control* ctl, uint32_t modules, int64_t start,
+                 int64_t end, int64_t step, int32_t nsteps, uint32_t flags) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (nsteps < 1) return fail(LT_ERR_ARG, "nsteps %d < 1", nsteps);
+  if ((modules & (M_TURB | M_MESO | M_CONVECTION)) && ctl->rng_mode == RNG_FAITHFUL)
+    return fail(LT_ERR_ARG, "faithful draws need the per-step stream state: use lt_run per step");
+  // one launch for the production chain with an in-kernel counter or Philox
+  // generator; anything else runs as nsteps single-step launches
+  const bool multi = modules == (M_TIMESTEPS | M_ADVECTION | M_TURB | M_MESO | M_POSITION) &&
+                     (flags & LT_RUN_RNG_INKERNEL) &&
+                     (ctl->rng_mode == RNG_COUNTER || ctl->rng_mode == RNG_PHILOX);
+  if (!multi) {
+    for (int32_t k = 0; k < nsteps; ++k)
+      if ((rc = run_impl(c, ctl, modules, start, end, step + k, 1, 0, 0, flags))) return rc;
+    return LT_OK;
+  }
+  // a pending sort rides along with the first step alone
+  if (c->pending && nsteps > 1) {
+    if ((rc = run_impl(c, ctl, modules, start, end, step, 1, 0, 0, flags))) return rc;
+    ++step;
+    --nsteps;
+  }
+  return run_impl(c, ctl, modules, start, end, step, nsteps, 0, 0, flags);
+}
+
+static int run_impl(lt_ctx* c, const lt_control* ctl, uint32_t modules, int64_t start,
+                    int64_t end, int64_t step, int32_t nsteps, uint64_t fstate, int64_t fbase,
+                    uint32_t flags) {
   int rc = check_ctx(c);
   if (rc || (rc = check_particles(c))) return rc;
   if (!(0 <= start && start <= end && end <= c->cap))
@@ -852,11 +891,12 @@ int lt_run(lt_ctx* c, const lt_control* ctl, uint32_t modules, int64_t start, in
            c->pend_start == 0 && c->pend_n == c->cap;
     if (!fuse && (rc = settle(c))) return rc;
   }
+  if (fuse && nsteps > 1) return fail(LT_ERR_STATE, "a pending sort fuses with one step only");
   if (c->timing) CK(cudaEventRecord(c->ev_start, c->stream));
   if (end > start) {
     rc = c->prec == LT_MET_F64
-             ? run_typed<RecD>(c, ctl, modules, start, end, step, fstate, fbase, flags, fuse)
-             : run_typed<RecF>(c, ctl, modules, start, end, step, fstate, fbase, flags, fuse);
+             ? run_typed<RecD>(c, ctl, modules, start, end, step, fstate, fbase, flags, fuse, nsteps)
+             : run_typed<RecF>(c, ctl, modules, start, end, step, fstate, fbase, flags, fuse, nsteps);
     if (rc) return rc;
   }
   CK(cudaEventRecord(c->compute_mark, c->stream));

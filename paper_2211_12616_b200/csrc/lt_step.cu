@@ -12,7 +12,7 @@ constexpr uint32_t kChainAdvDiff = M_TIMESTEPS | M_ADVECTION | M_TURB | M_MESO |
 constexpr uint32_t kChainPlume = kChainAdvDiff | M_SEDI | M_DECAY;
 constexpr uint32_t kChainFull = kChainAdvDiff | M_CONVECTION | M_SEDI | M_DECAY | M_ISOSURF | M_METEO;
 
-template <class Rec, uint32_t FIXED, int FAST, int RM, bool PERM = false>
+template <class Rec, uint32_t FIXED, int FAST, int RM, int PM = 0>
 static cudaError_t launch_fixed(const StepArgs<Rec>& a, cudaStream_t st) {
   static int blocks_per_sm = 0;
   static int sms = 0;
@@ -20,7 +20,7 @@ static cudaError_t launch_fixed(const StepArgs<Rec>& a, cudaStream_t st) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, step_kernel<Rec, FIXED, FAST, RM, PERM>, LT_STEP_BLOCK, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, step_kernel<Rec, FIXED, FAST, RM, PM>, LT_STEP_BLOCK, 0);
     if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
   const int64_t n = a.end - a.start;
@@ -31,7 +31,7 @@ static cudaError_t launch_fixed(const StepArgs<Rec>& a, cudaStream_t st) {
 #endif
   const int64_t cap = static_cast<int64_t>(sms) * blocks_per_sm * LT_GRID_WAVES;
   if (grid > cap) grid = cap;
-  step_kernel<Rec, FIXED, FAST, RM, PERM><<<static_cast<unsigned>(grid), LT_STEP_BLOCK, 0, st>>>(a);
+  step_kernel<Rec, FIXED, FAST, RM, PM><<<static_cast<unsigned>(grid), LT_STEP_BLOCK, 0, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -40,9 +40,14 @@ static cudaError_t launch_prec(const StepArgs<Rec>& a, cudaStream_t st) {
   // the production chain gets its in-kernel generator fixed at compile time;
   // with a pending box-sort permutation it applies it on the fly
   if (a.perm) {
-    if (a.ctl.rng_mode == RNG_COUNTER) return launch_fixed<Rec, kChainAdvDiff, FAST, RNG_COUNTER, true>(a, st);
-    if (a.ctl.rng_mode == RNG_PHILOX) return launch_fixed<Rec, kChainAdvDiff, FAST, RNG_PHILOX, true>(a, st);
-    return launch_fixed<Rec, kChainAdvDiff, FAST, RNG_FAITHFUL, true>(a, st);
+    if (a.ctl.rng_mode == RNG_COUNTER) return launch_fixed<Rec, kChainAdvDiff, FAST, RNG_COUNTER, 1>(a, st);
+    if (a.ctl.rng_mode == RNG_PHILOX) return launch_fixed<Rec, kChainAdvDiff, FAST, RNG_PHILOX, 1>(a, st);
+    return launch_fixed<Rec, kChainAdvDiff, FAST, RNG_FAITHFUL, 1>(a, st);
+  }
+  // several steps per launch (lt_run_steps checked the chain and generator)
+  if (a.nsteps > 1) {
+    if (a.ctl.rng_mode == RNG_PHILOX) return launch_fixed<Rec, kChainAdvDiff, FAST, RNG_PHILOX, 2>(a, st);
+    return launch_fixed<Rec, kChainAdvDiff, FAST, RNG_COUNTER, 2>(a, st);
   }
   if (a.modules == kChainAdvDiff && (a.flags & F_RNG_INKERNEL)) {
     if (a.ctl.rng_mode == RNG_COUNTER) return launch_fixed<Rec, kChainAdvDiff, FAST, RNG_COUNTER>(a, st);

@@ -56,6 +56,7 @@ struct StepArgs {
   int32_t nq;
   uint32_t modules, flags;
   int64_t step;
+  int32_t nsteps;  // steps per launch (MULTI kernels: in-kernel counter/Philox draws)
   uint64_t faithful_state;
   int64_t faithful_base;
   unsigned long long* iso_nonconv;
@@ -272,15 +273,15 @@ template <> struct Ops<RecF, 2> : OpsFast<2> {};
 // RNG_PHILOX or RNG_FAITHFUL, no batch); RM = -1 decides at run time.
 template <class O, int RM, class Rec>
 __device__ __forceinline__ void draws(const StepArgs<Rec>& a, int64_t s, uint64_t gid, int stream,
-                                      double x[3]) {
+                                      double x[3], int64_t step) {
   const Control& ctl = a.ctl;
   if (RM == RNG_COUNTER) {
-    if (stream == 0) x[0] = to_unit(counter_word(ctl.rng_seed_global, a.step, gid, 0, 0));
-    else O::normals(ctl.rng_seed_global, a.step, gid, stream, x);
+    if (stream == 0) x[0] = to_unit(counter_word(ctl.rng_seed_global, step, gid, 0, 0));
+    else O::normals(ctl.rng_seed_global, step, gid, stream, x);
     return;
   }
   if (RM == RNG_PHILOX) {
-    philox_stream(ctl.rng_seed_global, a.step, gid, stream, x);
+    philox_stream(ctl.rng_seed_global, step, gid, stream, x);
     return;
   }
   if (RM == RNG_FAITHFUL) {
@@ -297,12 +298,12 @@ __device__ __forceinline__ void draws(const StepArgs<Rec>& a, int64_t s, uint64_
     return;
   }
   if (ctl.rng_mode == RNG_COUNTER) {
-    if (stream == 0) x[0] = to_unit(counter_word(ctl.rng_seed_global, a.step, gid, 0, 0));
-    else O::normals(ctl.rng_seed_global, a.step, gid, stream, x);
+    if (stream == 0) x[0] = to_unit(counter_word(ctl.rng_seed_global, step, gid, 0, 0));
+    else O::normals(ctl.rng_seed_global, step, gid, stream, x);
   } else if (ctl.rng_mode == RNG_FAITHFUL) {
     faithful_stream(a.faithful_state, gid - static_cast<uint64_t>(a.faithful_base), stream, x);
   } else {
-    philox_stream(ctl.rng_seed_global, a.step, gid, stream, x);
+    philox_stream(ctl.rng_seed_global, step, gid, stream, x);
   }
 }
 
@@ -314,9 +315,12 @@ __device__ __forceinline__ int64_t row_index(const StepArgs<Rec>& a, int64_t s, 
   return (a.home_mask & group) && a.ids ? static_cast<int64_t>(a.ids[src]) - a.home_base : s;
 }
 
-template <class Rec, uint32_t FIXED, int FAST, int RM, bool PERM>
+// PM: 0 one step, 1 one step applying a pending permutation (PERM), 2
+// a.nsteps steps per particle (MULTI)
+template <class Rec, uint32_t FIXED, int FAST, int RM, int PM>
 __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel(const StepArgs<Rec> a) {
   using O = Ops<Rec, FAST>;
+  constexpr bool PERM = PM == 1, MULTI = PM == 2;
   const uint32_t mods = FIXED ? FIXED : a.modules;
   const Control& ctl = a.ctl;
   // each block walks its own contiguous run of (box-sorted) particles tile
@@ -361,205 +365,217 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
     double time = ld_state(a.time + src), lon = ld_state(a.lon + src), lat = ld_state(a.lat + src),
            p = ld_state(a.p + src);
 
-    // physics.py:82-88 (module_timesteps)
-    double dt;
-    if ((mods & M_TIMESTEPS) || !(a.flags & F_DT_ARRAY)) {
-      dt = np_min(ctl.t_stop - time, ctl.dt_model);
-      dt = np_min(np_max(dt, 0.0), ctl.dt_model);
-      if ((mods & M_TIMESTEPS) && (a.flags & F_WRITE_DT)) a.dt[row_index(a, s, src, HOME_DT)] = dt;
-    } else {
-      dt = a.dt[row_index(a, s, src, HOME_DT)];
-    }
-    const bool act = dt > 0.0;
-
     // random draws (rng.py:156-181) are made where they are consumed, which
     // keeps them out of the registers live across the advection gathers —
     // except on the fast counter path, below
     const uint64_t gid = (RM >= 0 || (a.flags & F_RNG_INKERNEL)) && (want_turb || want_meso || want_conv)
                              ? (a.ids ? static_cast<uint64_t>(a.ids[src]) : static_cast<uint64_t>(s))
                              : 0ull;
-#ifndef LT_LATE_DRAWS
-    // fast path with a compile-time generator: the six normals are pure ALU
-    // work on the id, done (fp32, SFU) before the first gather so they fill
-    // issue slots the gathers leave idle
-    // (the exact path measured slower this way: its fp64 normals cost twice
-    // the registers)
-    constexpr bool kEarly = FAST != 0 && RM >= 0;
-    float early[6];
-    if (kEarly && act) {
-      if (RM == RNG_FAITHFUL) {
-        faithful_normals_fast(a.faithful_state, gid - static_cast<uint64_t>(a.faithful_base), early);
-      } else if (RM == RNG_PHILOX) {
-        philox_normals_fast(ctl.rng_seed_global, a.step, gid, early);
+
+    // nsteps consecutive steps of this particle with its state in registers
+    // (particles are independent within a step; the caller keeps the met
+    // pair valid for all of them)
+    const int nk = MULTI ? a.nsteps : 1;
+    bool meso_wrote = false;  // the (single) PERM step wrote the o_uvwp rows
+#pragma unroll 1
+    for (int ks = 0; ks < nk; ++ks) {
+      const int64_t stp = a.step + ks;
+      // physics.py:82-88 (module_timesteps)
+      double dt;
+      if ((mods & M_TIMESTEPS) || !(a.flags & F_DT_ARRAY)) {
+        dt = np_min(ctl.t_stop - time, ctl.dt_model);
+        dt = np_min(np_max(dt, 0.0), ctl.dt_model);
+        if ((mods & M_TIMESTEPS) && (a.flags & F_WRITE_DT)) a.dt[row_index(a, s, src, HOME_DT)] = dt;
       } else {
-        double z[3];
-        if (want_turb) {
-          O::normals(ctl.rng_seed_global, a.step, gid, 1, z);
-          early[0] = z[0]; early[1] = z[1]; early[2] = z[2];
-        }
-        if (want_meso) {
-          O::normals(ctl.rng_seed_global, a.step, gid, 2, z);
-          early[3] = z[0]; early[4] = z[1]; early[5] = z[2];
+        dt = a.dt[row_index(a, s, src, HOME_DT)];
+      }
+      const bool act = dt > 0.0;
+      if (PERM) meso_wrote = want_meso && act;
+
+#ifndef LT_LATE_DRAWS
+      // fast path with a compile-time generator: the six normals are pure ALU
+      // work on the id, done (fp32, SFU) before the first gather so they fill
+      // issue slots the gathers leave idle
+      // (the exact path measured slower this way: its fp64 normals cost twice
+      // the registers)
+      constexpr bool kEarly = FAST != 0 && RM >= 0;
+      float early[6];
+      if (kEarly && act) {
+        if (RM == RNG_FAITHFUL) {
+          faithful_normals_fast(a.faithful_state, gid - static_cast<uint64_t>(a.faithful_base), early);
+        } else if (RM == RNG_PHILOX) {
+          philox_normals_fast(ctl.rng_seed_global, stp, gid, early);
+        } else {
+          double z[3];
+          if (want_turb) {
+            O::normals(ctl.rng_seed_global, stp, gid, 1, z);
+            early[0] = z[0]; early[1] = z[1]; early[2] = z[2];
+          }
+          if (want_meso) {
+            O::normals(ctl.rng_seed_global, stp, gid, 2, z);
+            early[3] = z[0]; early[4] = z[1]; early[5] = z[2];
+          }
         }
       }
-    }
 #endif
 
-    // physics.py:225-235 (module_isosurf_init)
-    if ((mods & M_ISOSURF_INIT) && ctl.isosurf_mode != ISO_OFF) {
-      if (ctl.isosurf_mode == ISO_PRESSURE) {
-        a.iso_var[row_index(a, s, src, HOME_ISO)] = p;
-      } else {
+      // physics.py:225-235 (module_isosurf_init)
+      if ((mods & M_ISOSURF_INIT) && ctl.isosurf_mode != ISO_OFF) {
+        if (ctl.isosurf_mode == ISO_PRESSURE) {
+          a.iso_var[row_index(a, s, src, HOME_ISO)] = p;
+        } else {
+          double v[4];
+          O::sample(a.met, time, lon, lat, p, 8, v);
+          a.iso_var[row_index(a, s, src, HOME_ISO)] = v[3] * O::power(1000.0 / p, kKappa);
+        }
+      }
+
+      // physics.py:91-116 (module_advection): explicit midpoint.  The two
+      // stages share one (rolled) sample call site to keep the kernel small.
+      if ((mods & M_ADVECTION) && act) {
+        const double half = 0.5 * dt;
+        double ts = time, xs = lon, ys = lat, zs = p, h = half;
+#pragma unroll 1
+        for (int stage = 0; stage < 2; ++stage) {
+          // stage 0: midpoint from (lon, lat, p) with half a step;
+          // stage 1: full step from (lon, lat, p) with the midpoint winds
+          O::adv_stage(a.met, ts, xs, ys, zs, lon, lat, p, h);
+          ts = time + half;
+          h = dt;
+        }
+        lon = xs; lat = ys; p = zs;
+        time = time + dt;
+      }
+
+      constexpr uint32_t kNoColumn = 0xFFFFFFFFu;
+      uint32_t tcol = kNoColumn;  // lon/lat column of the turb T sample (reused by meso)
+
+      // physics.py:119-147 (module_diffusion_turb); the vertical part sees the
+      // post-hop lon/lat and pre-hop p (numpy view aliasing)
+      if (want_turb && act) {
+        double xt[3];
+#ifndef LT_LATE_DRAWS
+        if (kEarly) { xt[0] = early[0]; xt[1] = early[1]; xt[2] = early[2]; }
+        else
+#endif
+        draws<O, RM>(a, s, gid, 1, xt, stp);
+        if (turb_h) {
+          double sig = a.kc.turb_sx;
+          if (__builtin_expect(dt != a.kc.dt, 0)) sig = sqrt(2.0 * ctl.turb_dx * dt);
+          const double nlon = lon + O::over_cos(sig * xt[0] * kDegPerM, lat);
+          lat = lat + sig * xt[1] * kDegPerM;
+          lon = nlon;
+        }
+        if (turb_v) {
+          double v[4];
+          O::sample(a.met, time, lon, lat, p, 8, v, &tcol);
+          double sz = a.kc.turb_sz;
+          if (__builtin_expect(dt != a.kc.dt, 0)) sz = sqrt(2.0 * ctl.turb_dz * dt);
+          const double dz = sz * xt[2];
+          p = O::vertical_hop(p, v[3], dz);
+        }
+      }
+
+      // physics.py:150-188 (module_diffusion_meso): AR(1) with met0 cell spread
+      if (want_meso && act) {
+        double xm[3];
+#ifndef LT_LATE_DRAWS
+        if (kEarly) { xm[0] = early[3]; xm[1] = early[4]; xm[2] = early[5]; }
+        else
+#endif
+        draws<O, RM>(a, s, gid, 2, xm, stp);
+        // the vertical hop moved only p: the T sample's lon/lat column holds
+        const uint32_t r00 = tcol != kNoColumn ? O::cell_in_column(a.met, tcol, p)
+                                               : O::cell(a.met, lon, lat, p);
+        // the AR(1) state loads go out before the spread gather so the two
+        // latencies overlap
+        double prev[3];
+#pragma unroll
+        for (int f = 0; f < 3; ++f) prev[f] = ld_state(a.uvwp[f] + src);
+        double sig[3];
+        O::spreads(a.met, r00, sig);
+        double r = a.kc.meso_r, amp = a.kc.meso_amp;
+        if (__builtin_expect(dt != a.kc.dt, 0)) {
+          r = 1.0 - 2.0 * dt / ctl.met_dt;
+          r = np_min(np_max(r, 0.0), 1.0);
+          amp = sqrt(1.0 - r * r);
+        }
+        double pert[3];
+#pragma unroll
+        for (int f = 0; f < 3; ++f) {
+          const double sigma = ctl.turb_meso * sig[f];
+          pert[f] = r * prev[f] + amp * sigma * xm[f];
+          st_state((PERM ? a.o_uvwp[f] : a.uvwp[f]) + s, pert[f]);
+        }
+        const double nlon = lon + O::over_cos(pert[0] * dt * kDegPerM, lat);
+        lat = lat + pert[1] * dt * kDegPerM;
+        lon = nlon;
+        p = p + pert[2] * dt;
+      }
+
+      // physics.py:191-203 (module_convection)
+      if (want_conv && act) {
+        double xc[3];
+        draws<O, RM>(a, s, gid, 0, xc, stp);
+        if (p > ctl.conv_p_top && xc[0] < ctl.conv_prob)
+          p = O::conv_target(ctl, a.kc, xc[0]);
+      }
+
+      // physics.py:206-222 (module_sedi): Stokes settling
+      if ((mods & M_SEDI) && ctl.sedi_radius != 0.0 && act) {
         double v[4];
         O::sample(a.met, time, lon, lat, p, 8, v);
-        a.iso_var[row_index(a, s, src, HOME_ISO)] = v[3] * O::power(1000.0 / p, kKappa);
+        p = O::sedi_hop(ctl, p, v[3], dt);
       }
-    }
 
-    // physics.py:91-116 (module_advection): explicit midpoint.  The two
-    // stages share one (rolled) sample call site to keep the kernel small.
-    if ((mods & M_ADVECTION) && act) {
-      const double half = 0.5 * dt;
-      double ts = time, xs = lon, ys = lat, zs = p, h = half;
-#pragma unroll 1
-      for (int stage = 0; stage < 2; ++stage) {
-        // stage 0: midpoint from (lon, lat, p) with half a step;
-        // stage 1: full step from (lon, lat, p) with the midpoint winds
-        O::adv_stage(a.met, ts, xs, ys, zs, lon, lat, p, h);
-        ts = time + half;
-        h = dt;
+      // decay (new module): q[slot] *= exp(-dt / tau) while active
+      if ((mods & M_DECAY) && ctl.decay_tau > 0.0 && act && ctl.decay_slot >= 0 &&
+          ctl.decay_slot < a.nq) {
+        double* qs = a.q + static_cast<int64_t>(ctl.decay_slot) * a.cap + row_index(a, s, src, HOME_Q);
+        *qs = *qs * (dt == a.kc.dt ? a.kc.decay : exp(-dt / ctl.decay_tau));
       }
-      lon = xs; lat = ys; p = zs;
-      time = time + dt;
-    }
 
-    constexpr uint32_t kNoColumn = 0xFFFFFFFFu;
-    uint32_t tcol = kNoColumn;  // lon/lat column of the turb T sample (reused by meso)
-
-    // physics.py:119-147 (module_diffusion_turb); the vertical part sees the
-    // post-hop lon/lat and pre-hop p (numpy view aliasing)
-    if (want_turb && act) {
-      double xt[3];
-#ifndef LT_LATE_DRAWS
-      if (kEarly) { xt[0] = early[0]; xt[1] = early[1]; xt[2] = early[2]; }
-      else
-#endif
-      draws<O, RM>(a, s, gid, 1, xt);
-      if (turb_h) {
-        double sig = a.kc.turb_sx;
-        if (__builtin_expect(dt != a.kc.dt, 0)) sig = sqrt(2.0 * ctl.turb_dx * dt);
-        const double nlon = lon + O::over_cos(sig * xt[0] * kDegPerM, lat);
-        lat = lat + sig * xt[1] * kDegPerM;
-        lon = nlon;
-      }
-      if (turb_v) {
-        double v[4];
-        O::sample(a.met, time, lon, lat, p, 8, v, &tcol);
-        double sz = a.kc.turb_sz;
-        if (__builtin_expect(dt != a.kc.dt, 0)) sz = sqrt(2.0 * ctl.turb_dz * dt);
-        const double dz = sz * xt[2];
-        p = O::vertical_hop(p, v[3], dz);
-      }
-    }
-
-    // physics.py:150-188 (module_diffusion_meso): AR(1) with met0 cell spread
-    if (want_meso && act) {
-      double xm[3];
-#ifndef LT_LATE_DRAWS
-      if (kEarly) { xm[0] = early[3]; xm[1] = early[4]; xm[2] = early[5]; }
-      else
-#endif
-      draws<O, RM>(a, s, gid, 2, xm);
-      // the vertical hop moved only p: the T sample's lon/lat column holds
-      const uint32_t r00 = tcol != kNoColumn ? O::cell_in_column(a.met, tcol, p)
-                                             : O::cell(a.met, lon, lat, p);
-      // the AR(1) state loads go out before the spread gather so the two
-      // latencies overlap
-      double prev[3];
-#pragma unroll
-      for (int f = 0; f < 3; ++f) prev[f] = ld_state(a.uvwp[f] + src);
-      double sig[3];
-      O::spreads(a.met, r00, sig);
-      double r = a.kc.meso_r, amp = a.kc.meso_amp;
-      if (__builtin_expect(dt != a.kc.dt, 0)) {
-        r = 1.0 - 2.0 * dt / ctl.met_dt;
-        r = np_min(np_max(r, 0.0), 1.0);
-        amp = sqrt(1.0 - r * r);
-      }
-      double pert[3];
-#pragma unroll
-      for (int f = 0; f < 3; ++f) {
-        const double sigma = ctl.turb_meso * sig[f];
-        pert[f] = r * prev[f] + amp * sigma * xm[f];
-        st_state((PERM ? a.o_uvwp[f] : a.uvwp[f]) + s, pert[f]);
-      }
-      const double nlon = lon + O::over_cos(pert[0] * dt * kDegPerM, lat);
-      lat = lat + pert[1] * dt * kDegPerM;
-      lon = nlon;
-      p = p + pert[2] * dt;
-    }
-
-    // physics.py:191-203 (module_convection)
-    if (want_conv && act) {
-      double xc[3];
-      draws<O, RM>(a, s, gid, 0, xc);
-      if (p > ctl.conv_p_top && xc[0] < ctl.conv_prob)
-        p = O::conv_target(ctl, a.kc, xc[0]);
-    }
-
-    // physics.py:206-222 (module_sedi): Stokes settling
-    if ((mods & M_SEDI) && ctl.sedi_radius != 0.0 && act) {
-      double v[4];
-      O::sample(a.met, time, lon, lat, p, 8, v);
-      p = O::sedi_hop(ctl, p, v[3], dt);
-    }
-
-    // decay (new module): q[slot] *= exp(-dt / tau) while active
-    if ((mods & M_DECAY) && ctl.decay_tau > 0.0 && act && ctl.decay_slot >= 0 &&
-        ctl.decay_slot < a.nq) {
-      double* qs = a.q + static_cast<int64_t>(ctl.decay_slot) * a.cap + row_index(a, s, src, HOME_Q);
-      *qs = *qs * (dt == a.kc.dt ? a.kc.decay : exp(-dt / ctl.decay_tau));
-    }
-
-    // physics.py:238-264 (module_isosurf): applies to every particle
-    if ((mods & M_ISOSURF) && ctl.isosurf_mode != ISO_OFF) {
-      if (ctl.isosurf_mode == ISO_PRESSURE) {
-        p = a.iso_var[row_index(a, s, src, HOME_ISO)];
-      } else {
-        const double theta0 = a.iso_var[row_index(a, s, src, HOME_ISO)];
-        nonconv += O::isosurf_theta(a.met, time, lon, lat, p, theta0) ? 0ull : 1ull;
-      }
-    }
-
-    // physics.py:267-287 (module_position): pole reflection, lon wrap, clamp
-    if (mods & M_POSITION) {
-      while (fabs(lat) > 90.0) {
-        lat = (lat > 0.0 ? 1.0 : -1.0) * (180.0 - fabs(lat));
-        lon = lon + 180.0;
-      }
-      if (lon < -180.0 || lon >= 180.0) {
-        double m = fmod(lon + 180.0, 360.0);  // np.mod: result takes the divisor's sign
-        if (m != 0.0) {
-          if (m < 0.0) m += 360.0;
+      // physics.py:238-264 (module_isosurf): applies to every particle
+      if ((mods & M_ISOSURF) && ctl.isosurf_mode != ISO_OFF) {
+        if (ctl.isosurf_mode == ISO_PRESSURE) {
+          p = a.iso_var[row_index(a, s, src, HOME_ISO)];
         } else {
-          m = 0.0;
+          const double theta0 = a.iso_var[row_index(a, s, src, HOME_ISO)];
+          nonconv += O::isosurf_theta(a.met, time, lon, lat, p, theta0) ? 0ull : 1ull;
         }
-        lon = m - 180.0;
       }
-      p = np_min(np_max(p, ctl.p_top), ctl.p_surf);
-    }
 
-    // physics.py:290-301 (module_meteo): sample T,u,v and climatology
-    if (mods & M_METEO) {
-      double v[4];
-      O::sample(a.met, time, lon, lat, p, 11, v);
-      const int64_t qi = row_index(a, s, src, HOME_Q);
-      a.q[qi] = v[3];
-      a.q[a.cap + qi] = v[0];
-      a.q[2 * a.cap + qi] = v[1];
-      a.q[3 * a.cap + qi] = clim_hno3(a.clim, lat, p);
-      a.q[4 * a.cap + qi] = p < clim_ptrop(a.clim, lat) ? 1.0 : 0.0;
-    }
+      // physics.py:267-287 (module_position): pole reflection, lon wrap, clamp
+      if (mods & M_POSITION) {
+        while (fabs(lat) > 90.0) {
+          lat = (lat > 0.0 ? 1.0 : -1.0) * (180.0 - fabs(lat));
+          lon = lon + 180.0;
+        }
+        if (lon < -180.0 || lon >= 180.0) {
+          double m = fmod(lon + 180.0, 360.0);  // np.mod: result takes the divisor's sign
+          if (m != 0.0) {
+            if (m < 0.0) m += 360.0;
+          } else {
+            m = 0.0;
+          }
+          lon = m - 180.0;
+        }
+        p = np_min(np_max(p, ctl.p_top), ctl.p_surf);
+      }
+
+      // physics.py:290-301 (module_meteo): sample T,u,v and climatology
+      if (mods & M_METEO) {
+        double v[4];
+        O::sample(a.met, time, lon, lat, p, 11, v);
+        const int64_t qi = row_index(a, s, src, HOME_Q);
+        a.q[qi] = v[3];
+        a.q[a.cap + qi] = v[0];
+        a.q[2 * a.cap + qi] = v[1];
+        a.q[3 * a.cap + qi] = clim_hno3(a.clim, lat, p);
+        a.q[4 * a.cap + qi] = p < clim_ptrop(a.clim, lat) ? 1.0 : 0.0;
+      }
+
+    }  // steps
 
     if (mods & (M_ADVECTION | M_TURB | M_MESO | M_CONVECTION | M_SEDI | M_ISOSURF | M_POSITION)) {
       st_state((PERM ? a.o_p : a.p) + s, p);
@@ -575,7 +591,7 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
         st_state(a.o_lat + s, lat);
       }
       if (!(mods & M_ADVECTION)) st_state(a.o_time + s, time);
-      if (!(want_meso && act)) {
+      if (!meso_wrote) {
 #pragma unroll
         for (int f = 0; f < 3; ++f) st_state(a.o_uvwp[f] + s, ld_state(a.uvwp[f] + src));
       }

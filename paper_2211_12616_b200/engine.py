@@ -180,6 +180,19 @@ class Engine:
                      faithful_base=self.first_id, flags=capi.RUN_RNG_INKERNEL)
         self._last_modules = modules
 
+    def step_many(self, ctl, step: int, nsteps: int, modules: int = ADV_DIFF) -> None:
+        """`nsteps` fused steps of every particle (lt_run_steps: the
+        production chain in one launch, state in registers across the steps;
+        identical results).  The bound met pair must cover all of them — call
+        between rotations.  Faithful draws step one launch at a time here
+        (their per-step stream state lives on the host)."""
+        if nsteps <= 1 or ctl.rng_mode == "faithful":
+            for k in range(nsteps):
+                self.step(ctl, step + k, modules)
+            return
+        self.ctx.run_steps(ctl, modules, 0, self.n, step, nsteps, flags=capi.RUN_RNG_INKERNEL)
+        self._last_modules = modules
+
     def step_host(self, ctl, ens, cache, step: int, modules: int = ADV_DIFF,
                   device_id: int = 0, chunk: int = 0, steps: int = 1) -> None:
         """`steps` fused steps (step, step+1, ...) of a HOST ensemble (numpy

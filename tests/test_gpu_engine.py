@@ -468,3 +468,35 @@ def test_fast_path_regional_irregular_grid(eng, same_time):
     assert np.abs(fast.lat - exact.lat).max() / 180.0 <= 1e-5
     assert (np.abs(fast.p - exact.p) / exact.p).max() <= 1e-5
     np.testing.assert_array_equal(fast.time, exact.time)
+
+
+@pytest.mark.parametrize("precision,rng_mode", [("exact", "counter"), ("fast", "philox"),
+                                                ("fast", "counter")])
+def test_multi_step_launch_equals_single_steps(eng, precision, rng_mode):
+    """Engine.step_many (lt_run_steps: each particle advanced K steps in one
+    launch, state in registers) == K single-step launches, bit for bit —
+    including after a box sort whose permutation rides along with the first
+    step."""
+    engine, ms, syn = eng
+    m0, m1 = syn.analytic_pair(1.0, 1.0, 60, 0.0, 10800.0)
+    ens = syn.particles(30_000, seed=5)
+    ctl = ms.Control(t_stop=5400.0, dt_model=180.0, met_dt=10800.0, rng_mode=rng_mode,
+                     rng_seed_global=9, precision=precision)
+    outs = []
+    for many in (False, True):
+        e = engine.Engine(device=0)
+        e.upload(ens)
+        e.bind_met(m0, m1)
+        step = 0
+        for cycle in range(3):
+            e.sort(engine.ADV_DIFF)
+            if many:
+                e.step_many(ctl, step, 7, engine.ADV_DIFF)
+            else:
+                for k in range(7):
+                    e.step(ctl, step + k, engine.ADV_DIFF)
+            step += 7
+        out = e.download()
+        outs.append(np.stack([out.lon, out.lat, out.p, out.time]))
+        e.close()
+    np.testing.assert_array_equal(outs[1], outs[0])
