@@ -140,7 +140,9 @@ def run_simulation(ctl, ens, mets, num_devices: int = 1, *, fused: bool = True,
 
         t = ctl.t_start
         next_out = ctl.t_start + ctl.output_dt
-        for step in range(n_steps_for(ctl)):
+        n_steps = n_steps_for(ctl)
+        step = 0
+        while step < n_steps:
             t_next = min(t + ctl.dt_model, ctl.t_stop)
             while met1.t_met < t_next:      # driver_cli.py:139-149
                 if not rest:
@@ -163,15 +165,29 @@ def run_simulation(ctl, ens, mets, num_devices: int = 1, *, fused: bool = True,
                 if fused:
                     prefetch_all()
 
+            # fused mode runs the steps up to the next event (met rotation,
+            # box sort, output) as one multi-step launch (Engine.step_many:
+            # identical results, each particle advanced in registers)
+            run, t_end = 1, t_next
             if fused:
-                def device_step(d, step=step):
+                while step + run < n_steps:
+                    t_more = min(t_end + ctl.dt_model, ctl.t_stop)
+                    if (met1.t_met < t_more or (sort_every and (step + run) % sort_every == 0)
+                            or t_end >= next_out - _OUT_EPS or t_end >= ctl.t_stop):
+                        break
+                    run, t_end = run + 1, t_more
+            if fused:
+                def device_step(d, step=step, run=run):
                     img = regions[d].image
                     if sort_every and step % sort_every == 0:
                         img.engine.sort(modules)
                     ctx = img.engine.ctx
                     ctx.timing(True)
-                    img.engine.step(img.ctl, step, modules, device_id=d,
-                                    num_devices=num_devices)
+                    if run > 1:
+                        img.engine.step_many(img.ctl, step, run, modules, device_id=d)
+                    else:
+                        img.engine.step(img.ctl, step, modules, device_id=d,
+                                        num_devices=num_devices)
                     ms = ctx.last_elapsed_ms()
                     ctx.timing(False)
                     timers.record("module_fused_step", "PHYSICS", device_scope(d),
@@ -181,7 +197,8 @@ def run_simulation(ctl, ens, mets, num_devices: int = 1, *, fused: bool = True,
                     _module_step(regions[d].image, ranges[d], d, step, t_next, rng,
                                  met0, met1, timers)
             pool.for_each_device_parallel(device_step, parallel=parallel)
-            t = t_next
+            t = t_end
+            step += run
 
             if t >= next_out - _OUT_EPS or t >= ctl.t_stop:   # driver_cli.py:188-195
                 for d in range(num_devices):

@@ -180,7 +180,8 @@ class Engine:
                      faithful_base=self.first_id, flags=capi.RUN_RNG_INKERNEL)
         self._last_modules = modules
 
-    def step_many(self, ctl, step: int, nsteps: int, modules: int = ADV_DIFF) -> None:
+    def step_many(self, ctl, step: int, nsteps: int, modules: int = ADV_DIFF,
+                  device_id: int = 0) -> None:
         """`nsteps` fused steps of every particle (lt_run_steps: the
         production chain in one launch, state in registers across the steps;
         identical results).  The bound met pair must cover all of them — call
@@ -188,7 +189,7 @@ class Engine:
         (their per-step stream state lives on the host)."""
         if nsteps <= 1 or ctl.rng_mode == "faithful":
             for k in range(nsteps):
-                self.step(ctl, step + k, modules)
+                self.step(ctl, step + k, modules, device_id=device_id)
             return
         self.ctx.run_steps(ctl, modules, 0, self.n, step, nsteps, flags=capi.RUN_RNG_INKERNEL)
         self._last_modules = modules

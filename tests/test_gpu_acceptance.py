@@ -207,3 +207,40 @@ def test_driver_edge_cases(m):
     np.testing.assert_array_equal(outs[0], outs[1])
     with pytest.raises(ValueError):
         driver.run_simulation(ms.Control(t_stop=7200.0), syn.particles(10), mets)
+
+
+def test_driver_multi_step_runs_equal_single_steps(m, golden_chain, monkeypatch):
+    """run_simulation(fused) advances the steps between events (met rotation,
+    sort, output) as multi-step launches; the result equals one launch per
+    step bit for bit, with outputs and rotations inside the run."""
+    ms, driver = m["ms"], m["driver"]
+    from paper_2211_12616_b200 import engine as eng
+    g = golden_chain
+    mets = [snapshot_from(g, "m0"), snapshot_from(g, "m1")]
+    ctl = ms.Control(t_stop=9000.0, dt_model=180.0, met_dt=10800.0, rng_mode="counter",
+                     output_dt=1800.0)
+
+    def run():
+        ens = ms.ParticleEnsemble(np=g["init_p"].size, time=g["init_time"].copy(),
+                                  p=g["init_p"].copy(), zeta=g["init_zeta"].copy(),
+                                  lon=g["init_lon"].copy(), lat=g["init_lat"].copy(),
+                                  q=g["init_q"].copy())
+        outs = []
+        status, _ = driver.run_simulation(ctl, ens, mets, num_devices=2, fused=True,
+                                          modules=eng.ADV_DIFF, sort_every=7,
+                                          on_output=lambda c, e, cache, t: outs.append(
+                                              (t, e.lon.copy())))
+        assert status == 0
+        return np.stack([ens.lon, ens.lat, ens.p, ens.time]), outs
+
+    multi, outs_m = run()
+
+    def single(self, ctl, step, nsteps, modules=eng.ADV_DIFF, device_id=0):
+        for k in range(nsteps):
+            self.step(ctl, step + k, modules, device_id=device_id)
+    monkeypatch.setattr(eng.Engine, "step_many", single)
+    ref, outs_r = run()
+    np.testing.assert_array_equal(multi, ref)
+    assert [t for t, _ in outs_m] == [t for t, _ in outs_r] and len(outs_m) == 5
+    for (_, a), (_, b) in zip(outs_m, outs_r):
+        np.testing.assert_array_equal(a, b)
