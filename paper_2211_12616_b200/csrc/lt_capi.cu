@@ -856,18 +856,29 @@ int lt_run_steps(lt_ctx* c, const lt_control* ctl, uint32_t modules, int64_t sta
   const bool multi = modules == (M_TIMESTEPS | M_ADVECTION | M_TURB | M_MESO | M_POSITION) &&
                      (flags & LT_RUN_RNG_INKERNEL) &&
                      (ctl->rng_mode == RNG_COUNTER || ctl->rng_mode == RNG_PHILOX);
+  // the event timing (lt_timing) spans every launch of the call
+  const bool timing = c->timing;
+  if (timing) CK(cudaEventRecord(c->ev_start, c->stream));
+  c->timing = false;
   if (!multi) {
-    for (int32_t k = 0; k < nsteps; ++k)
-      if ((rc = run_impl(c, ctl, modules, start, end, step + k, 1, 0, 0, flags))) return rc;
-    return LT_OK;
+    for (int32_t k = 0; k < nsteps && !rc; ++k)
+      rc = run_impl(c, ctl, modules, start, end, step + k, 1, 0, 0, flags);
+  } else {
+    // a pending sort rides along with the first step alone
+    if (c->pending && nsteps > 1) {
+      rc = run_impl(c, ctl, modules, start, end, step, 1, 0, 0, flags);
+      ++step;
+      --nsteps;
+    }
+    if (!rc) rc = run_impl(c, ctl, modules, start, end, step, nsteps, 0, 0, flags);
   }
-  // a pending sort rides along with the first step alone
-  if (c->pending && nsteps > 1) {
-    if ((rc = run_impl(c, ctl, modules, start, end, step, 1, 0, 0, flags))) return rc;
-    ++step;
-    --nsteps;
+  c->timing = timing;
+  if (rc) return rc;
+  if (timing) {
+    CK(cudaEventRecord(c->ev_stop, c->stream));
+    c->timed_once = true;
   }
-  return run_impl(c, ctl, modules, start, end, step, nsteps, 0, 0, flags);
+  return LT_OK;
 }
 
 static int run_impl(lt_ctx* c, const lt_control* ctl, uint32_t modules, int64_t start,
