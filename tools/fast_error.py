@@ -1,5 +1,6 @@
-"""Distribution of fast-vs-exact run differences (test_fast_precision shape):
-    LAGTRANS_B200_LIB=... python tools/fast_error.py"""
+"""Distribution of fast-vs-exact run differences over 24 h (480 steps):
+    python tools/fast_error.py [counter|philox] [cfg2|cfg3]
+(cfg2: the test's 1 deg shape; cfg3: the headline 0.25 deg x 137 grid)."""
 import sys
 from pathlib import Path
 
@@ -23,11 +24,16 @@ def run(ctl, m0, m1, ens, steps, sort_every=40):
     return out
 
 
-m0, m1 = synthetic.analytic_pair(1.0, 1.0, 60, 0.0, 10800.0)
-ens = synthetic.particles(200_000, seed=21)
 mode = sys.argv[1] if len(sys.argv) > 1 else "counter"
+shape = sys.argv[2] if len(sys.argv) > 2 else "cfg2"
+if shape == "cfg3":   # the headline grid: 0.25 deg x 137 levels, 1e6 particles
+    m0, m1 = synthetic.analytic_pair(0.25, 0.25, 137, 0.0, 10800.0, p_min=0.01)
+    ens = synthetic.particles(1_000_000, seed=21)
+else:                 # the test's shape: 1 deg x 60 levels, 2e5 particles
+    m0, m1 = synthetic.analytic_pair(1.0, 1.0, 60, 0.0, 10800.0)
+    ens = synthetic.particles(200_000, seed=21)
 kw = dict(t_stop=86400.0, dt_model=180.0, met_dt=10800.0, rng_mode=mode, rng_seed_global=5)
-print("rng", mode)
+print("rng", mode, "shape", shape)
 ex = run(ms.Control(**kw), m0, m1, ens, 480)
 fa = run(ms.Control(precision="fast", **kw), m0, m1, ens, 480)
 rp = np.abs(fa.p - ex.p) / ex.p
