@@ -27,7 +27,7 @@ static cudaError_t launch_fixed(const StepArgs<Rec>& a, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   int64_t grid = (n + LT_STEP_BLOCK - 1) / LT_STEP_BLOCK;
 #ifndef LT_GRID_WAVES
-#define LT_GRID_WAVES 16
+#define LT_GRID_WAVES 48
 #endif
   const int64_t cap = static_cast<int64_t>(sms) * blocks_per_sm * LT_GRID_WAVES;
   if (grid > cap) grid = cap;
