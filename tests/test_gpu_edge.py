@@ -95,3 +95,35 @@ def test_bad_arguments_raise_reference_types(m):
     with pytest.raises(capi.LifecycleError):
         ctx.sort_by_box(0, 10)                                 # sort needs met
     ctx.close()
+
+
+def test_run_steps_arguments(m):
+    """lt_run_steps: nsteps < 1 and faithful draws (whose stream state is per
+    step on the host) are argument errors; a non-production chain runs as
+    single steps and matches them."""
+    capi, ms, syn, engine = m["capi"], m["ms"], m["syn"], m["engine"]
+    m0, m1 = syn.analytic_pair(dlon=30.0, dlat=30.0, nlev=6)
+    ens = syn.particles(500, seed=2)
+    e = engine.Engine(device=0)
+    e.upload(ens)
+    e.bind_met(m0, m1)
+    with pytest.raises(ValueError):
+        e.ctx.run_steps(ms.Control(rng_mode="counter"), engine.ADV_DIFF, 0, 500, 0, 0,
+                        flags=capi.RUN_RNG_INKERNEL)
+    with pytest.raises(ValueError):
+        e.ctx.run_steps(ms.Control(rng_mode="faithful"), engine.ADV_DIFF, 0, 500, 0, 3,
+                        flags=capi.RUN_RNG_INKERNEL)
+    ctl = ms.Control(rng_mode="counter")
+    adv = engine.modules_mask(["advection", "position"])
+    e.ctx.run_steps(ctl, adv, 0, 500, 0, 4)
+    got = e.download()
+    e.close()
+    f = engine.Engine(device=0)
+    f.upload(ens)
+    f.bind_met(m0, m1)
+    for k in range(4):
+        f.ctx.run(ctl, adv, 0, 500, step=k)
+    ref = f.download()
+    f.close()
+    for k in ("lon", "lat", "p", "time"):
+        np.testing.assert_array_equal(getattr(got, k), getattr(ref, k))
