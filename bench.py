@@ -6,7 +6,7 @@
 Headline workload (BASELINE.json configs[2], the configuration the metric is
 quoted on): **cfg3** — 1e8 particles on the synthetic ERA5-like 0.25 deg grid
 (1440(+1) x 721 x 137), advection + turbulent + mesoscale diffusion
-(+ timesteps, in-kernel counter RNG, position), sharded over N GPUs with the
+(+ timesteps, in-kernel Philox draws, position), sharded over N GPUs with the
 reference partition rule, met replicated to every rank by an NCCL
 broadcast.  A "step" is one fused time step of every particle; the box sort
 runs every `--sort-every` steps (15 for cfg3, the measured optimum of
@@ -33,8 +33,10 @@ by the full 32-bit particle id — the reference's splitmix64 counter key
 packs only 24 bits of index, so at 1e8 particles it would hand particles i
 and i + 2^24 identical draws; `counter` reproduces the reference's words
 bit for bit.  The line also carries the same measurement with the
-bit-faithful "exact" kernels (`alt_precision`) and with the counter words
-(`alt_rng`).
+bit-faithful "exact" kernels (`alt_precision`), with the counter words
+(`alt_rng`), and with the steps between two sorts run as one multi-step
+launch each (`alt_multistep`, Engine.step_many; identical results).  The
+headline is one launch per step, the unit its roofline is stated for.
 """
 
 from __future__ import annotations
