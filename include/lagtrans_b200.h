@@ -164,7 +164,8 @@ int lt_run(lt_ctx *ctx, const lt_control *ctl, uint32_t modules, int64_t start,
            int64_t faithful_base, uint32_t flags);
 /* nsteps consecutive steps; results identical to nsteps lt_run calls.  The
    production chain (timesteps|advection|turb|meso|position) with in-kernel
-   counter or philox draws runs as one launch, each particle's state held in
+   counter or philox draws, and the advection chain (timesteps|advection|
+   position), run as one launch, each particle's state held in
    registers across the steps (a pending box-sort permutation is applied by
    a first single step); anything else as nsteps launches.  The selected met
    pair must cover all the steps. */

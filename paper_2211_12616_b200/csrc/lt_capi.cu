@@ -853,9 +853,10 @@ int lt_run_steps(lt_ctx* c, const lt_control* ctl, uint32_t modules, int64_t sta
     return fail(LT_ERR_ARG, "faithful draws need the per-step stream state: use lt_run per step");
   // one launch for the production chain with an in-kernel counter or Philox
   // generator; anything else runs as nsteps single-step launches
-  const bool multi = modules == (M_TIMESTEPS | M_ADVECTION | M_TURB | M_MESO | M_POSITION) &&
-                     (flags & LT_RUN_RNG_INKERNEL) &&
-                     (ctl->rng_mode == RNG_COUNTER || ctl->rng_mode == RNG_PHILOX);
+  const bool multi =
+      modules == (M_TIMESTEPS | M_ADVECTION | M_POSITION) ||
+      (modules == (M_TIMESTEPS | M_ADVECTION | M_TURB | M_MESO | M_POSITION) &&
+       (flags & LT_RUN_RNG_INKERNEL) && (ctl->rng_mode == RNG_COUNTER || ctl->rng_mode == RNG_PHILOX));
   // the event timing (lt_timing) spans every launch of the call
   const bool timing = c->timing;
   if (timing) CK(cudaEventRecord(c->ev_start, c->stream));

@@ -46,6 +46,7 @@ static cudaError_t launch_prec(const StepArgs<Rec>& a, cudaStream_t st) {
   }
   // several steps per launch (lt_run_steps checked the chain and generator)
   if (a.nsteps > 1) {
+    if (a.modules == kChainAdv) return launch_fixed<Rec, kChainAdv, FAST, -1, 2>(a, st);
     if (a.ctl.rng_mode == RNG_PHILOX) return launch_fixed<Rec, kChainAdvDiff, FAST, RNG_PHILOX, 2>(a, st);
     return launch_fixed<Rec, kChainAdvDiff, FAST, RNG_COUNTER, 2>(a, st);
   }
