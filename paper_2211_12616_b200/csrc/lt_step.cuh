@@ -449,6 +449,10 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
 
       constexpr uint32_t kNoColumn = 0xFFFFFFFFu;
       uint32_t tcol = kNoColumn;  // lon/lat column of the turb T sample (reused by meso)
+      // exact Philox: the turb and meso normals share block 1 and a pair,
+      // so both streams are drawn at the turb step (meso's kept till then)
+      constexpr bool kBoth = !kEarly && RM == RNG_PHILOX && ((FIXED & (M_TURB | M_MESO)) == (M_TURB | M_MESO));
+      double zmeso[3] = {0.0, 0.0, 0.0};
 
       // physics.py:119-147 (module_diffusion_turb); the vertical part sees the
       // post-hop lon/lat and pre-hop p (numpy view aliasing)
@@ -458,7 +462,8 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
         if (kEarly) { xt[0] = early[0]; xt[1] = early[1]; xt[2] = early[2]; }
         else
 #endif
-        draws<O, RM>(a, s, gid, 1, xt, stp);
+        if (kBoth) philox_turb_meso(ctl.rng_seed_global, stp, gid, xt, zmeso);
+        else draws<O, RM>(a, s, gid, 1, xt, stp);
         if (turb_h) {
           double sig = a.kc.turb_sx;
           if (__builtin_expect(dt != a.kc.dt, 0)) sig = sqrt(2.0 * ctl.turb_dx * dt);
@@ -483,7 +488,8 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
         if (kEarly) { xm[0] = early[3]; xm[1] = early[4]; xm[2] = early[5]; }
         else
 #endif
-        draws<O, RM>(a, s, gid, 2, xm, stp);
+        if (kBoth && want_turb) { xm[0] = zmeso[0]; xm[1] = zmeso[1]; xm[2] = zmeso[2]; }
+        else draws<O, RM>(a, s, gid, 2, xm, stp);
         // the vertical hop moved only p: the T sample's lon/lat column holds
         const uint32_t r00 = tcol != kNoColumn ? O::cell_in_column(a.met, tcol, p)
                                                : O::cell(a.met, lon, lat, p);
