@@ -48,7 +48,7 @@ struct AxisHost {
   int logscale = 0;
   float g0 = 0.f, ginv = 0.f;
   int uniform = 0;
-  double dinv = 0.0;
+  double dinv = 0.0, dorg = 0.0;
 };
 
 struct Slot {
@@ -152,6 +152,7 @@ int upload_axis(AxisHost& ax, const double* x, int n, cudaStream_t st) {
   ax.hi = x[n - 1];
   ax.uniform = lin <= 1e-9 ? 1 : 0;
   ax.dinv = (n - 1) / (x[n - 1] - x[0]);
+  ax.dorg = -x[0] * ax.dinv;
   if (ax.dev && ax.n != n) {
     cudaFree(ax.dev);
     cudaFree(ax.cell);
@@ -192,6 +193,7 @@ Axis view(const AxisHost& a) {
   v.ginv = a.ginv;
   v.uniform = a.uniform;
   v.dinv = a.dinv;
+  v.dorg = a.dorg;
   return v;
 }
 
