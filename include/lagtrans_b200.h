@@ -206,6 +206,12 @@ int lt_rng_fill(lt_ctx *ctx, int32_t mode, uint64_t seed_or_state, int64_t step,
 /* interpolate_met (physics.py:69-79) at n host points: out = u,v,w,T rows (4n) */
 int lt_interpolate(lt_ctx *ctx, int64_t n, const double *t, const double *lon,
                    const double *lat, const double *p, double *out);
+/* the cell lookup of the exact (precision 0) or fast (1, f32 store) kernels
+   at n host points: out = i, j, k rows (3n int32), which must equal the
+   reference's _locate (physics.py:31-47: searchsorted(side='left') - 1,
+   clipped; reversed levels) — the box-index audit; needs lt_met_grid only */
+int lt_locate_cells(lt_ctx *ctx, int32_t precision, int64_t n, const double *lon,
+                    const double *lat, const double *p, int32_t *out);
 /* theta-isosurface non-convergence counter (CacheState.iso_nonconverged) */
 int lt_iso_counter(lt_ctx *ctx, int64_t *value, int32_t reset);
 

@@ -117,6 +117,7 @@ _PROTOS = {
     "lt_met_copy_slot": ([_P, _I32, _P, _I32], C.c_int),
     "lt_met_slot_time": ([_P, _I32, C.POINTER(_D)], C.c_int),
     "lt_clim_load": ([_P, _I32, _I32, _P, _P, _P, _P], C.c_int),
+    "lt_locate_cells": ([_P, _I32, _I64, _P, _P, _P, _P], C.c_int),
     "lt_run": ([_P, C.POINTER(LtControl), _U32, _I64, _I64, _I64, _U64, _I64, _U32], C.c_int),
     "lt_run_steps": ([_P, C.POINTER(LtControl), _U32, _I64, _I64, _I64, _I32, _U32], C.c_int),
     "lt_rng_fill": ([_P, _I32, _U64, _I64, _I64, _I64], C.c_int),

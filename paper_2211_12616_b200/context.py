@@ -298,6 +298,16 @@ class DeviceContext:
                                            capi.ptr(p), capi.ptr(out)))
         return out
 
+    def locate_cells(self, lon, lat, p, precision: str = "exact") -> np.ndarray:
+        """(3, n) int32 cell indices (i, j, k) of the exact or fast kernels'
+        lookup at host points (lt_locate_cells; the box-index audit)."""
+        lon, lat, p = _f64(lon), _f64(lat), _f64(p)
+        out = np.empty((3, lon.size), dtype=np.int32)
+        capi.check(self.lib.lt_locate_cells(self.h, capi.PRECISIONS[precision], lon.size,
+                                            capi.ptr(lon), capi.ptr(lat), capi.ptr(p),
+                                            capi.ptr(out)))
+        return out
+
     def timing(self, on: bool) -> None:
         capi.check(self.lib.lt_timing(self.h, int(on)))
 

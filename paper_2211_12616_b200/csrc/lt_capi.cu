@@ -1098,6 +1098,50 @@ int lt_interpolate(lt_ctx* c, int64_t n, const double* t, const double* lon, con
   return LT_OK;
 }
 
+// the cell lookup of the exact (precision 0) or fast (1) kernels at n host
+// points: out = i, j, k rows (3n int32) — the cell audit against the
+// reference's _locate (physics.py:31-47); needs the grid only
+int lt_locate_cells(lt_ctx* c, int32_t precision, int64_t n, const double* lon, const double* lat,
+                    const double* p, int32_t* out) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (!c->nx) return fail(LT_ERR_STATE, "met grid not set");
+  if (precision != 0 && precision != 1) return fail(LT_ERR_ARG, "precision must be 0 or 1");
+  if (precision == 1 && c->prec != LT_MET_F32)
+    return fail(LT_ERR_ARG, "the fast kernels run on the f32 met store only");
+  if (n < 0) return fail(LT_ERR_ARG, "negative point count");
+  if (n == 0) return LT_OK;
+  char* buf = nullptr;
+  if ((rc = alloc_dev(reinterpret_cast<void**>(&buf), (sizeof(double) * 3 + sizeof(int32_t) * 3) * n,
+                      "locate points")))
+    return rc;
+  double* d = reinterpret_cast<double*>(buf);
+  int32_t* o = reinterpret_cast<int32_t*>(buf + sizeof(double) * 3 * n);
+  const double* src[3] = {lon, lat, p};
+  cudaError_t e = cudaSuccess;
+  for (int f = 0; f < 3 && e == cudaSuccess; ++f)
+    e = cudaMemcpyAsync(d + f * n, src[f], sizeof(double) * n, cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess) {
+    if (c->prec == LT_MET_F64) {
+      MetView<RecD> m{};
+      m.lon = view(c->ax_lon); m.lat = view(c->ax_lat); m.lev = view(c->ax_lev);
+      m.ny = c->ny; m.nz = c->nz;
+      e = launch_locate<RecD>(m, precision, d, d + n, d + 2 * n, o, n, c->stream);
+    } else {
+      MetView<RecF> m{};
+      m.lon = view(c->ax_lon); m.lat = view(c->ax_lat); m.lev = view(c->ax_lev);
+      m.ny = c->ny; m.nz = c->nz;
+      e = launch_locate<RecF>(m, precision, d, d + n, d + 2 * n, o, n, c->stream);
+    }
+  }
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(out, o, sizeof(int32_t) * 3 * n, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  cudaFree(buf);
+  CK(e);
+  return LT_OK;
+}
+
 // ------------------------------------------------------------------ sort
 
 extern "C++" {

@@ -148,6 +148,30 @@ __global__ void sample_kernel(MetView<Rec> m, const double* t, const double* lon
   }
 }
 
+// physics.py:31-47 cell lookup alone, for the cell audit (lt_locate_cells):
+// FAST = 0 the exact bracketing every exact kernel uses (cell_of), 1 / 2
+// the fast kernels' lookups (cell_fast<G>) on any / a geographic grid
+template <class Rec, int FAST>
+__global__ void locate_kernel(MetView<Rec> m, const double* lon, const double* lat,
+                              const double* p, int32_t* out, int64_t n) {
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int i, j, k;
+    if constexpr (FAST == 0) {
+      const Cell c = cell_of(m, lon[t], lat[t], p[t]);
+      i = c.i; j = c.j; k = c.k;
+    } else {
+      const CellF c = cell_fast<FAST>(m, lon[t], lat[t], p[t]);
+      i = static_cast<int>(c.col / m.ny);
+      j = static_cast<int>(c.col % m.ny);
+      k = static_cast<int>(c.r00 - c.col * static_cast<uint32_t>(m.nz - 1));
+    }
+    out[t] = i;
+    out[n + t] = j;
+    out[2 * n + t] = k;
+  }
+}
+
 __global__ void iota_kernel(uint32_t* ids, int64_t offset, int64_t count, int64_t first) {
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < count;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -246,6 +270,25 @@ cudaError_t launch_sample(const MetView<Rec>& m, const double* t, const double* 
 }
 template cudaError_t launch_sample<RecF>(const MetView<RecF>&, const double*, const double*, const double*, const double*, double*, int64_t, cudaStream_t);
 template cudaError_t launch_sample<RecD>(const MetView<RecD>&, const double*, const double*, const double*, const double*, double*, int64_t, cudaStream_t);
+
+template <class Rec>
+cudaError_t launch_locate(const MetView<Rec>& m, int fast, const double* lon, const double* lat,
+                          const double* p, int32_t* out, int64_t n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  if (fast == 0) {
+    locate_kernel<Rec, 0><<<grid_for(n), 256, 0, st>>>(m, lon, lat, p, out, n);
+  } else if constexpr (sizeof(Rec) == sizeof(RecF)) {
+    // the same dispatch as launch_step: geographic grids get the G = 2 lookups
+    const bool geo = m.lon.uniform && m.lat.uniform && !m.lev.uniform && m.lev.logscale;
+    if (geo) locate_kernel<Rec, 2><<<grid_for(n), 256, 0, st>>>(m, lon, lat, p, out, n);
+    else locate_kernel<Rec, 1><<<grid_for(n), 256, 0, st>>>(m, lon, lat, p, out, n);
+  } else {
+    return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+template cudaError_t launch_locate<RecF>(const MetView<RecF>&, int, const double*, const double*, const double*, int32_t*, int64_t, cudaStream_t);
+template cudaError_t launch_locate<RecD>(const MetView<RecD>&, int, const double*, const double*, const double*, int32_t*, int64_t, cudaStream_t);
 
 cudaError_t launch_iota(uint32_t* ids, int64_t offset, int64_t count, int64_t first, cudaStream_t st) {
   if (count <= 0) return cudaSuccess;

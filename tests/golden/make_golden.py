@@ -104,18 +104,28 @@ def gen_interp():
                         **met_arrays("m0", m0), **met_arrays("m1", m1))
 
 
+def modules_control():
+    return Control(np_max=10**6, t_stop=9000.0, met_dt=10800.0, turb_dx=50.0,
+                   turb_dz=0.1, turb_meso=0.16, conv_prob=0.3, conv_p_top=300.0,
+                   sedi_radius=5e-6, sedi_density=2000.0, isosurf_mode="theta",
+                   rng_mode="counter", rng_seed_global=12616)
+
+
 def gen_modules():
     """Single-call in/out pairs for every module from identical inputs."""
     lons, lats, levs = grid(10.0, 5.0, np.geomspace(1013.25, 1.0, 20))
     m0 = analytic_met(0.0, lons, lats, levs)
     m1 = analytic_met(10800.0, lons, lats, levs, phase=10.0)
-    ctl = Control(np_max=10**6, t_stop=9000.0, met_dt=10800.0, turb_dx=50.0,
-                  turb_dz=0.1, turb_meso=0.16, conv_prob=0.3, conv_p_top=300.0,
-                  sedi_radius=5e-6, sedi_density=2000.0, isosurf_mode="theta",
-                  rng_mode="counter", rng_seed_global=12616)
-    n = 3000
-    ens = particles(ctl, n, 11)
-    rs = np.random.default_rng(12)
+    ctl = modules_control()
+    ens = particles(ctl, 3000, 11)
+    np.savez_compressed(OUT / "modules.npz", **module_pairs(ctl, m0, m1, ens))
+
+
+def module_pairs(ctl, m0, m1, ens, seed=12, lon_span=(-900.0, 900.0)):
+    """Every module called once, in pipeline order, on the reference; the
+    ensemble before and after each call (plus the batch it drew)."""
+    n = ens.np
+    rs = np.random.default_rng(seed)
     ens.time[:] = f32(rs.uniform(0.0, 9000.0, n))
     ens.time[:50] = 9000.0           # finished particles
     ens.time[50:100] = 8950.0        # partial final step
@@ -156,7 +166,7 @@ def gen_modules():
     physics.module_isosurf(ctl, ens, m0, m1, cache, work); snap("isosurf")
     rec["iso_nonconverged"] = cache.iso_nonconverged
     ens.lat[:200] = f32(rs.uniform(-300.0, 300.0, 200))   # pole reflections
-    ens.lon[:400] = f32(rs.uniform(-900.0, 900.0, 400))   # wraps
+    ens.lon[:400] = f32(rs.uniform(*lon_span, 400))        # wraps
     ens.lon[400:410] = [180.0, -180.0, 540.0, -540.0, 179.99998, -180.00002,
                         360.0, 0.0, -0.0, 720.0]
     ens.p[400:420] = f32(rs.uniform(0.0, 1200.0, 20)); snap("preposition")
@@ -166,7 +176,51 @@ def gen_modules():
     physics.module_isosurf_init(ctl_p, ens, m0, m1, cache, work)
     ens.p[:] = ens.p + 3.0
     physics.module_isosurf(ctl_p, ens, m0, m1, cache, work); snap("isopressure")
-    np.savez_compressed(OUT / "modules.npz", **rec)
+    return rec
+
+
+def gen_hires():
+    """The headline grid's shape (0.25 deg, all 137 levels down to 0.01 hPa)
+    on a 40 x 40 deg window (hires_met.py): every module once from
+    identical inputs (module_pairs), and a 20-step advection + turbulent +
+    mesoscale diffusion + position chain with the reference's counter draws
+    (the production chain), 1e4 particles each."""
+    sys.path.insert(0, str(OUT))
+    import hires_met as hm
+    lons, lats, levs = hm.axes()
+    f0, f1 = hm.fields(lons, lats, levs, 0.0), hm.fields(lons, lats, levs, 5.0)
+    m0 = MeteoField(t_met=0.0, lons=lons, lats=lats, levs=levs, **f0)
+    m1 = MeteoField(t_met=10800.0, lons=lons, lats=lats, levs=levs, **f1)
+    m0.validate(); m1.validate()
+    n = 10000
+
+    def cloud(ctl, seed):
+        rs = np.random.default_rng(seed)
+        ens = ensemble_allocate(ctl, n)
+        ens.lon[:] = f32(rs.uniform(-180.5, -139.5, n))   # a few outside the window
+        ens.lat[:] = f32(rs.uniform(-90.0, -50.5, n))
+        p = rs.uniform(300.0, 900.0, n)                     # cfg3's particles
+        k = n // 10
+        p[:3 * k] = np.exp(rs.uniform(np.log(0.01), np.log(1013.25), 3 * k))  # every level
+        p[3 * k:4 * k] = rs.choice(levs, k)                 # exact level nodes
+        p[4 * k:5 * k] = rs.uniform(0.001, 1100.0, k)       # incl. beyond the hull
+        ens.p[:] = f32(p)
+        return ens
+
+    ctl = modules_control()
+    rec = module_pairs(ctl, m0, m1, cloud(ctl, 31), seed=32, lon_span=(-400.0, 400.0))
+    rec = {f"mod_{k}": v for k, v in rec.items() if not k.startswith(("m0_", "m1_"))}
+    cctl = Control(np_max=10**6, t_stop=86400.0, dt_model=180.0, met_dt=10800.0,
+                   turb_dx=50.0, turb_dz=0.1, turb_meso=0.16, rng_mode="counter",
+                   rng_seed_global=2211)
+    ens = cloud(cctl, 33)
+    init = ens_arrays("chain_init", ens)
+    cache = run_chain(cctl, ens, m0, m1, None, 20, ("advection", "turb", "meso", "position"))
+    np.savez_compressed(OUT / "hires.npz", lons=lons, lats=lats, levs=levs,
+                        digest0=np.array(hm.fields_digest(f0)),
+                        digest1=np.array(hm.fields_digest(f1)),
+                        **rec, **init, **ens_arrays("chain_final", ens),
+                        chain_final_uvwp=cache.uvwp)
 
 
 def gen_rng():
@@ -307,7 +361,7 @@ def gen_output():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["interp", "modules", "rng", "chain", "sbr", "output"]
+    which = sys.argv[1:] or ["interp", "modules", "rng", "chain", "sbr", "output", "hires"]
     for name in which:
         globals()[f"gen_{name}"]()
         print("wrote", name)
