@@ -87,8 +87,16 @@ WORKLOADS = {
                  desc="5e8 particles, full module chain (+decay) with box sort every 10 "
                       "steps"),
 }
-# algorithmic state bytes per particle-step (fp64 rows read + written)
-STATE_BYTES = {ADV: 64, ADV_DIFF: 112, PLUME: 128, FULL: 168}
+# algorithmic state bytes per particle-step, SURVEY.md 8(d) ("fp64
+# lon/lat/p/time + fp32 uvwp" column): lon/lat/p/time read + written (64 B),
+# + the meso AR(1) state uvwp as fp32 read + written (24 B), + for the
+# longer chains the decayed q slot read + written (16 B) and, for the full
+# chain, iso_var read (8 B) and q0..4 written (40 B)
+STATE_BYTES = {ADV: 64, ADV_DIFF: 88, PLUME: 104, FULL: 152}
+# what this implementation's rows actually move per particle-step: uvwp is
+# kept in fp64 (the reference's CacheState dtype; the exact kernels need it),
+# i.e. +24 B over 8(d), plus the 4-byte particle-id row (RNG key) once sorted
+MOVED_STATE_BYTES = {ADV: 64, ADV_DIFF: 116, PLUME: 132, FULL: 180}
 
 
 def dist_env():
@@ -157,8 +165,23 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+def pure_modules():
+    """(synthetic, model_state) loaded WITHOUT the package's __init__ (which
+    loads liblagtrans_b200.so): the --impl reference arm builds the same
+    inputs with no product code mapped into the process."""
+    import importlib
+    import types
+    name = "_lt_inputs"
+    if name not in sys.modules:
+        pkg = types.ModuleType(name)
+        pkg.__path__ = [str(ROOT / "paper_2211_12616_b200")]
+        sys.modules[name] = pkg
+    return importlib.import_module(name + ".synthetic"), importlib.import_module(name + ".model_state")
+
+
 def make_ctl(wl, precision="fast", rng_mode="counter"):
-    from paper_2211_12616_b200.model_state import Control
+    _, ms = pure_modules()
+    Control = ms.Control
     cfg = WORKLOADS[wl]
     kw = dict(np_max=10 ** 10, t_stop=30 * 86400.0, dt_model=180.0,
               met_dt=cfg.get("met_dt", 10800.0), turb_dx=50.0, turb_dz=0.1, turb_meso=0.16,
@@ -168,7 +191,7 @@ def make_ctl(wl, precision="fast", rng_mode="counter"):
 
 
 def make_particles(wl, n, seed):
-    from paper_2211_12616_b200 import synthetic
+    synthetic, _ = pure_modules()
     cfg = WORKLOADS[wl]
     nq = cfg.get("ctl", {}).get("nq", 5)
     if cfg["init"] == "point":
@@ -183,7 +206,7 @@ def make_particles(wl, n, seed):
 def build_met(wl, rank, ws):
     """Rank 0 (or the only rank) builds the first snapshot pair on the host;
     other ranks only need the grid (the fields arrive by broadcast)."""
-    from paper_2211_12616_b200 import synthetic
+    synthetic, _ = pure_modules()
     cfg = WORKLOADS[wl]
     dlon, dlat, nlev, pmin = cfg["grid"]
     if cfg["met"] == "sbr":
@@ -288,6 +311,30 @@ def cpu_sample_rate(wl, mets, ctl, n_sample, steps, threads, target_s=0.0):
     return n_sample * steps / wall, wall, n_sample
 
 
+def pcie_duplex_gbs(torch, gpu, gib=1):
+    """Measured host-link ceiling: pinned H2D and D2H of `gib` GiB running
+    at once on two streams (the e2e path's traffic pattern); GB/s per
+    direction, best of 3."""
+    n = (gib << 30) // 8
+    h1 = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    h2 = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    d1 = torch.empty(n, dtype=torch.float64, device=f"cuda:{gpu}")
+    d2 = torch.empty(n, dtype=torch.float64, device=f"cuda:{gpu}")
+    s1, s2 = torch.cuda.Stream(gpu), torch.cuda.Stream(gpu)
+    best = 1e9
+    for _ in range(3):
+        torch.cuda.synchronize(gpu)
+        t0 = time.perf_counter()
+        with torch.cuda.stream(s1):
+            d1.copy_(h1, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h2.copy_(d2, non_blocking=True)
+        torch.cuda.synchronize(gpu)
+        best = min(best, time.perf_counter() - t0)
+    del h1, h2, d1, d2
+    return n * 8 / best / 1e9
+
+
 def host_threads():
     try:
         return len(os.sched_getaffinity(0))
@@ -312,19 +359,146 @@ def run_reference(args, wl):
         r, wall, n_used = cpu_sample_rate(wl, mets, ctl, n_sample, 2, threads, target_s=10.0)
         rates.append(r)
     v = statistics.median(rates)
+    try:   # the arm must not have mapped any product library (checked, reported)
+        maps = Path("/proc/self/maps").read_text()
+        product_loaded = "liblagtrans_b200" in maps
+    except OSError:
+        product_loaded = None
     print(json.dumps({
-        "impl": "reference", "metric": METRIC, "value": v, "unit": "particle-steps/s",
+        "impl": "reference", "product_code_loaded": product_loaded, "metric": METRIC, "value": v, "unit": "particle-steps/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * n_job / v, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": wl, "description": cfg["desc"], "particles": n_job},
+        "config": {"workload": wl, "description": cfg["desc"], "particles": n_job,
+                   "modules": list(cfg["chain"]), "precision": "exact (numpy fp64, the "
+                   "reference's operation sequence)", "rng": "counter (reference splitmix64 "
+                   "words)", "parallelism": f"{threads} host threads, DevicePool-style static "
+                   "partition (device_runtime.py:136-161)"},
         "cpu_baseline": {"value": v, "unit": "particle-steps/s", "cores": threads,
                          "kind": "port",
-                         "sample": f"{n_used} particles x 2 steps per repeat on the same met "
-                                   f"grid, {len(rates)} repeats (median)"},
+                         "sample": f"{n_used} particles x 2 steps per repeat on the same "
+                                   f"{wl} met grid, {len(rates)} repeats (median); "
+                                   "ms_per_step is the sample rate scaled to the "
+                                   "workload's particle count"},
         "e2e": {"value": v, "unit": "particle-steps/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }), flush=True)
+
+
+def run_one_process(args, wl):
+    """--gpus N without torchrun: ONE process drives N GPUs (the paper's
+    design, arXiv 2211.12616 / device_runtime.DevicePool): one Engine and one
+    host thread per GPU, particles sharded by calc_device_workload_range,
+    met uploaded once to GPU 0 and replicated by lt_met_broadcast (one NCCL
+    broadcast group over NVLink/NVSwitch).  Timing: CUDA events on every
+    engine's stream after a common barrier, max over GPUs.  (More devices
+    than GPUs present share them round-robin: the functional path on a
+    single-GPU box, where the broadcast degenerates to device-local copies.)"""
+    import torch
+    from concurrent.futures import ThreadPoolExecutor
+
+    from paper_2211_12616_b200 import engine
+    from paper_2211_12616_b200.context import met_broadcast, nccl_info
+    from paper_2211_12616_b200.partition import partition_all
+    cfg = WORKLOADS[wl]
+    G = args.gpus
+    ngpu = torch.cuda.device_count()
+    devs = [d % ngpu for d in range(G)]
+    n_tot = cfg["n"] * (G if args.scaling == "weak" else 1)
+    ranges = partition_all(n_tot, G)
+    mask = engine.modules_mask(cfg["chain"])
+    ctl = make_ctl(wl, args.precision, args.rng)
+    m0, m1 = build_met(wl, 0, 1)
+    pool = ThreadPoolExecutor(G)
+    engs = [None] * G
+
+    def setup(d):
+        torch.cuda.set_device(devs[d])
+        w = ranges[d]
+        e = engine.Engine(device=devs[d], first_id=w.start, nq=ctl.nq)
+        e.upload(make_particles(wl, w.size, 12616 + d))
+        e.set_grid(m0.lons, m0.lats, m0.levs)
+        engs[d] = e
+    list(pool.map(setup, range(G)))
+    # met: one host upload (GPU 0), one broadcast per snapshot to the others
+    t0 = time.perf_counter()
+    engs[0].ctx.load_met(0, m0, key="m0")
+    engs[0].ctx.load_met(1, m1, key="m1")
+    if G > 1:
+        for slot in (0, 1):
+            met_broadcast([e.ctx for e in engs], 0, [slot] * G)
+    for e in engs:
+        e.ctx.use_met(0, 1)
+        e._met_slots, e._staged = (0, 1), None
+        e.sync()
+    t_met = time.perf_counter() - t0
+    sort_every = args.sort_every if args.sort_every >= 0 else cfg["sort_every"]
+    state = {"step": 0}
+
+    def steps(d, k, ev=None):
+        torch.cuda.set_device(devs[d])
+        e = engs[d]
+        st = state["step"]
+        sh = torch.cuda.ExternalStream(e.ctx.stream_handle())
+        if ev:
+            ev[0].record(sh)
+        for i in range(k):
+            if sort_every and (st + i) % sort_every == 0:
+                e.sort(mask)
+            e.step(ctl, st + i, mask, device_id=d)
+        if ev:
+            ev[1].record(sh)
+        e.sync()
+
+    def run(k, timed=False):
+        evs = None
+        if timed:
+            evs = []
+            for d in range(G):
+                with torch.cuda.device(devs[d]):
+                    evs.append([torch.cuda.Event(enable_timing=True) for _ in range(2)])
+        list(pool.map(lambda d: steps(d, k, evs[d] if evs else None), range(G)))
+        state["step"] += k
+        return max(ev[0].elapsed_time(ev[1]) for ev in evs) if evs else None
+
+    run(args.warmup)
+    with ClockSampler(devs[0]) as clk:
+        total_ms = run(args.steps, timed=True)
+    value = n_tot * args.steps / (total_ms / 1e3)
+    dlon, dlat, nlev, pmin = cfg["grid"]
+    nodes = (int(round(360.0 / dlon)) + 1) * (int(round(180.0 / dlat)) + 1) * nlev
+    b = algorithmic_bytes(cfg["chain"], ranges[0].size, nodes)
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
+        if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    peak = peaks.get("hbm_gbs", 6650.0)
+    per_gpu_ms = total_ms / args.steps
+    achieved = b * ranges[0].size / (per_gpu_ms / 1e3) / 1e9
+    info = nccl_info()
+    print(json.dumps({
+        "metric": METRIC, "value": value, "unit": "particle-steps/s", "n_gpus": G,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_gpu_ms,
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+        "dtype": "f64 state / f32 interpolation" if args.precision == "fast" else "f64",
+        "data": "synthetic",
+        "config": {"workload": wl, "description": cfg["desc"], "particles": n_tot,
+                   "particles_per_gpu": ranges[0].size, "modules": list(cfg["chain"]),
+                   "precision": args.precision, "rng": args.rng, "sort_every": sort_every,
+                   "parallelism": f"one process drives {G} GPUs (threads), particles sharded "
+                                  f"(calc_device_workload_range), met replicated by "
+                                  "lt_met_broadcast (NCCL), no data-path collective",
+                   "devices": devs, "l2": "inputs larger than L2"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "kernel": "step_kernel (per GPU, "
+                     "ms/step incl. sorts)", "algorithmic_bytes_per_particle_step": b},
+        "met_broadcast": {"nccl_version": info["version"], "nccl_ranks": info["ranks"],
+                          "gpus_distinct": len(set(devs)),
+                          "setup_s_upload_plus_broadcast": t_met},
+        "clocks": clk.summary(),
+        "gpu_launches": args.steps * G + G * sum(1 for i in range(args.steps)
+                                                 if sort_every and (args.warmup + i) % sort_every == 0) * 7,
+    }), flush=True)
+    for e in engs:
+        e.close()
 
 
 def main():
@@ -345,14 +519,18 @@ def main():
     ap.add_argument("--precision", default="fast", choices=("exact", "fast"))
     ap.add_argument("--met-store", default="f32", choices=("f32", "f64"))
     ap.add_argument("--rng", default="philox", choices=("counter", "faithful", "philox"))
-    ap.add_argument("--scaling", default="weak", choices=("weak", "strong"),
-                    help="weak: each GPU advances the workload's particle count; strong: "
-                         "the workload's total is sharded over the GPUs")
+    ap.add_argument("--scaling", default="strong", choices=("weak", "strong"),
+                    help="strong (default, BASELINE cfg3: 1e8 sharded over 1/2/4/8 GPUs): "
+                         "the workload's total is sharded over the GPUs; weak: each GPU "
+                         "advances the workload's particle count")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     wl = args.workload
     if args.impl == "reference":
         run_reference(args, wl)
+        return
+    if args.gpus > 1 and dist_env()[0] == 1:
+        run_one_process(args, wl)
         return
 
     import torch
@@ -479,12 +657,18 @@ def main():
                 "roofline_frac": b * work.size / (k2 / 1e3) / 1e9 / peak, "steps": k,
                 "clocks": clk2}
 
-    other = alt_rng = None
+    other = alt_rng = alt_ref = None
     k_other = args.steps if args.alt_steps < 0 else args.alt_steps
     if k_other > 0:
         other = alt_run("exact" if args.precision == "fast" else "fast", args.rng, k_other)
         if args.rng != "counter":
             alt_rng = alt_run(args.precision, "counter", k_other)
+        if (args.precision, args.rng) != ("exact", "counter") and \
+                (other["precision"], other["rng"]) != ("exact", "counter"):
+            # the fully reference-faithful configuration: numpy-exact fp64
+            # kernels fed the reference's own counter words (like for like
+            # with the --impl reference arm)
+            alt_ref = alt_run("exact", "counter", k_other)
 
     # the same steps with the sort cadence, but every run of steps between
     # two sorts is one multi-step launch (Engine.step_many: each particle
@@ -562,9 +746,15 @@ def main():
             (1 if "decay" in chain else 0)
         rows_out = 4 + (3 if "meso" in chain else 0) + \
             (5 if "meteo" in chain else (1 if "decay" in chain else 0))
+        bw = pcie_duplex_gbs(torch, gpu)
+        h2d_b, d2h_b = 8 * rows_in * n_tot, 8 * rows_out * n_tot
+        ceiling = n_tot / (max(h2d_b, d2h_b) / ws / (bw * 1e9))
         e2e = {"value": n_tot * args.e2e_steps / te, "unit": "particle-steps/s",
-               "h2d_bytes_per_step": 8 * rows_in * n_tot, "d2h_bytes_per_step": 8 * rows_out * n_tot,
+               "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b,
                "steps": args.e2e_steps,
+               "bound": "host link (PCIe): every step moves the state rows in and out",
+               "pcie_duplex_gbs_per_direction": bw, "pcie_ceiling": ceiling,
+               "frac_of_pcie_ceiling": n_tot * args.e2e_steps / te / ceiling,
                "path": "Engine.step_host(steps=K) -> lt_run_host_steps: pinned host SoA, every "
                        "step chunked H2D / fused step / D2H on three streams, pipelined across "
                        "steps (wall clock, max over ranks)"}
@@ -626,10 +816,17 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "step_kernel", "kernel_ms": kern_avg,
-                         "algorithmic_bytes_per_particle_step": b, "issue": issue,
+                         "algorithmic_bytes_per_particle_step": b,
+                         "algorithmic_bytes_source": "SURVEY.md 8(d): b_state (fp64 "
+                         "lon/lat/p/time + fp32 uvwp column) + b_met = 32*nodes*(1-exp(-8N/"
+                         "nodes))/N",
+                         "moved_bytes_per_particle_step": MOVED_STATE_BYTES[cfg["chain"]] +
+                         b - STATE_BYTES[cfg["chain"]],
+                         "issue": issue,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks
                          else "fallback"},
-            "alt_precision": other, "alt_rng": alt_rng, "alt_multistep": multi,
+            "alt_precision": other, "alt_rng": alt_rng, "alt_reference_faithful": alt_ref,
+            "alt_multistep": multi,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": launches,
         }), flush=True)

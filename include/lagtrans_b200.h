@@ -152,6 +152,20 @@ int lt_met_use(lt_ctx *ctx, int32_t slot0, int32_t slot1);
    met broadcast replacing the per-device deep copies of
    device_runtime.py:178-186; both contexts must hold the same grid */
 int lt_met_copy_slot(lt_ctx *dst, int32_t dst_slot, lt_ctx *src, int32_t src_slot);
+/* the met broadcast of the one-process-drives-all-GPUs design
+   (arXiv 2211.12616; replaces the deep copy of met0/met1 into every device
+   image on each rotation, driver_cli.py:146-149 -> device_runtime.py:178-186):
+   slot slots[root] of ctxs[root] is replicated into slot slots[i] of every
+   other context by ONE ncclBroadcast group over the distinct GPUs (NCCL is
+   loaded at run time, communicators from ncclCommInitAll, cached per device
+   list), each rank on its context's copy stream; contexts sharing a GPU get
+   a device-to-device copy.  Asynchronous: lt_met_use orders the compute
+   stream after the transfer, as after lt_met_load. */
+int lt_met_broadcast(lt_ctx *const *ctxs, int32_t n, int32_t root, const int32_t *slots);
+/* NCCL version code of the loaded libnccl (LT_ERR_STATE if none loads) and
+   the number of NCCL ranks the process has created */
+int lt_nccl_version(int32_t *version);
+int lt_nccl_ranks(int32_t *nranks);
 int lt_met_slot_time(lt_ctx *ctx, int32_t slot, double *t_met);
 
 /* climatology tables for module_meteo (ClimData model_state.py:156-181) */

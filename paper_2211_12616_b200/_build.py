@@ -19,8 +19,9 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIBDIR = PKG / "_lib"
 LIB = LIBDIR / "liblagtrans_b200.so"
-SOURCES = ["lt_capi.cu", "lt_kernels.cu", "lt_step.cu", "lt_output.cu", "lt_host.cpp"]
-HEADERS = ["lt_device.cuh", "lt_step.cuh", "lt_kernels.cuh"]
+SOURCES = ["lt_capi.cu", "lt_kernels.cu", "lt_step.cu", "lt_output.cu", "lt_host.cpp",
+           "lt_comm.cu"]
+HEADERS = ["lt_device.cuh", "lt_step.cuh", "lt_kernels.cuh", "lt_comm.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "--expt-relaxed-constexpr",
          "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-v"]
@@ -42,13 +43,19 @@ def _stale() -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
+LAST_MODE = None   # "compiled" | "up-to-date" (the shipped .so is newer than every source)
+
+
 def build(force: bool = False, verbose: bool = False, outdir: Path | None = None,
           defines: tuple[str, ...] = ()) -> Path:
     """Compile and link; `outdir`/`defines` build an experimental variant."""
     libdir = Path(outdir) if outdir else LIBDIR
     lib = libdir / LIB.name
+    global LAST_MODE
     if not force and outdir is None and not defines and not _stale():
+        LAST_MODE = "up-to-date"
         return LIB
+    LAST_MODE = "compiled"
     libdir.mkdir(parents=True, exist_ok=True)
 
     def compile_one(src):
@@ -68,7 +75,7 @@ def build(force: bool = False, verbose: bool = False, outdir: Path | None = None
     objs = [o for o, _ in results]
     log = [text for _, text in results]
     tmp = lib.with_suffix(".so.tmp")
-    cmd = [nvcc(), *ARCH, "-shared", "--cudart", "static", "-o", str(tmp), *objs, "-lpthread"]
+    cmd = [nvcc(), *ARCH, "-shared", "--cudart", "static", "-o", str(tmp), *objs, "-lpthread", "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")

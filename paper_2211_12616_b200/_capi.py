@@ -115,6 +115,9 @@ _PROTOS = {
     "lt_met_load_nodes": ([_P, _I32, _D, _P, _U32], C.c_int),
     "lt_met_use": ([_P, _I32, _I32], C.c_int),
     "lt_met_copy_slot": ([_P, _I32, _P, _I32], C.c_int),
+    "lt_met_broadcast": ([C.POINTER(_P), _I32, _I32, C.POINTER(_I32)], C.c_int),
+    "lt_nccl_version": ([C.POINTER(_I32)], C.c_int),
+    "lt_nccl_ranks": ([C.POINTER(_I32)], C.c_int),
     "lt_met_slot_time": ([_P, _I32, C.POINTER(_D)], C.c_int),
     "lt_clim_load": ([_P, _I32, _I32, _P, _P, _P, _P], C.c_int),
     "lt_locate_cells": ([_P, _I32, _I64, _P, _P, _P, _P], C.c_int),

@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "../../include/lagtrans_b200.h"
+#include "lt_comm.cuh"
 #include "lt_kernels.cuh"
 
 using namespace lt;
@@ -697,6 +698,21 @@ int lt_met_use(lt_ctx* c, int32_t s0, int32_t s1) {
   return LT_OK;
 }
 
+// Direct peer access dst -> src (NVLink), so peer copies do not stage
+// through host memory; a no-op when the pair cannot (the copy then still
+// works, through the driver's staging).  Leaves dst's device current.
+static int enable_peer(int dst, int src) {
+  int can = 0;
+  CK(cudaDeviceCanAccessPeer(&can, dst, src));
+  if (can) {
+    CK(cudaSetDevice(dst));
+    cudaError_t e = cudaDeviceEnablePeerAccess(src, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();  // clear the sticky-free error
+    else CK(e);
+  }
+  return LT_OK;
+}
+
 // Replicate a packed snapshot GPU to GPU (NVLink peer copy, or a D2D copy
 // when both contexts share a GPU): the single-process counterpart of the
 // met broadcast.  The copy runs on the destination's copy stream after the
@@ -711,16 +727,118 @@ int lt_met_copy_slot(lt_ctx* dst, int32_t dslot, lt_ctx* src, int32_t sslot) {
   if ((rc = met_prepare(dst, dslot))) return rc;  // also orders after dst's compute
   const size_t bytes = rec_bytes(src) * n_rec(src);
   CK(cudaStreamWaitEvent(dst->copy, src->slots[sslot].ready, 0));
-  if (dst->device == src->device)
+  if (dst->device == src->device) {
     CK(cudaMemcpyAsync(dst->slots[dslot].rec, src->slots[sslot].rec, bytes, cudaMemcpyDeviceToDevice, dst->copy));
-  else
+  } else {
+    if ((rc = enable_peer(dst->device, src->device))) return rc;
     CK(cudaMemcpyPeerAsync(dst->slots[dslot].rec, dst->device, src->slots[sslot].rec, src->device, bytes, dst->copy));
+  }
   CK(cudaEventRecord(dst->slots[dslot].ready, dst->copy));
   // the source slot must not be refilled (on src's copy stream) before this
   // copy has read it
   CK(cudaStreamWaitEvent(src->copy, dst->slots[dslot].ready, 0));
   dst->slots[dslot].t_met = src->slots[sslot].t_met;
   dst->slots[dslot].valid = true;
+  return LT_OK;
+}
+
+// The met broadcast of the one-process design: slot slots[root] of
+// ctxs[root] reaches slot slots[i] of every other context.  Distinct GPUs
+// receive it by ONE ncclBroadcast group (NVLink / NVSwitch, each rank on its
+// context's copy stream); further contexts on an already-served GPU (test
+// setups mapping several devices onto one B200) get a device-to-device copy
+// from the context that received it there.  Every destination slot is
+// ordered after that context's compute work (met_prepare) and its ready event
+// follows the transfer, exactly as for an upload.
+int lt_met_broadcast(lt_ctx* const* ctxs, int32_t n, int32_t root, const int32_t* slots) {
+  if (!ctxs || !slots || n < 1) return fail(LT_ERR_ARG, "lt_met_broadcast needs n >= 1 contexts and slots");
+  if (root < 0 || root >= n) return fail(LT_ERR_ARG, "broadcast root %d outside [0, %d)", root, n);
+  lt_ctx* src = ctxs[root];
+  int rc = check_ctx(src);
+  if (rc) return rc;
+  const int sslot = slots[root];
+  if (sslot < 0 || sslot > 2) return fail(LT_ERR_ARG, "met slot %d outside [0, 3)", sslot);
+  if (!src->slots[sslot].valid) return fail(LT_ERR_STATE, "root met slot %d not loaded", sslot);
+  for (int i = 0; i < n; ++i) {
+    lt_ctx* d = ctxs[i];
+    if (!d) return fail(LT_ERR_STATE, "null context %d (deleted region?)", i);
+    if (d->nx != src->nx || d->ny != src->ny || d->nz != src->nz || d->prec != src->prec)
+      return fail(LT_ERR_ARG, "met grid of context %d differs from the root's (call lt_met_grid first)", i);
+    for (int j = 0; j < i; ++j)
+      if (ctxs[j] == d) return fail(LT_ERR_ARG, "context %d appears twice in the broadcast", i);
+  }
+  const size_t bytes = rec_bytes(src) * n_rec(src);
+  // one representative per GPU (the root's GPU: the root itself)
+  std::vector<int> rep_of(n, -1), devs, reps;
+  devs.push_back(src->device);
+  reps.push_back(root);
+  rep_of[root] = root;
+  for (int i = 0; i < n; ++i) {
+    if (i == root) continue;
+    auto it = std::find(devs.begin(), devs.end(), ctxs[i]->device);
+    if (it == devs.end()) {
+      devs.push_back(ctxs[i]->device);
+      reps.push_back(i);
+      rep_of[i] = i;
+    } else {
+      rep_of[i] = reps[it - devs.begin()];
+    }
+  }
+  for (int i = 0; i < n; ++i) {
+    if (i == root) continue;
+    if ((rc = check_ctx(ctxs[i])) || (rc = met_prepare(ctxs[i], slots[i]))) return rc;
+  }
+  // the root's copy stream sends once the root slot is packed (it is its own stream)
+  CK(cudaSetDevice(src->device));
+  CK(cudaStreamWaitEvent(src->copy, src->slots[sslot].ready, 0));
+  if (devs.size() > 1) {
+    std::vector<void*> bufs;
+    std::vector<cudaStream_t> streams;
+    for (int r : reps) {
+      bufs.push_back(ctxs[r]->slots[slots[r]].rec);
+      streams.push_back(ctxs[r]->copy);
+    }
+    std::string err;
+    if (lt_comm::broadcast(devs, bufs, bytes, 0, streams, &err))
+      return fail(LT_ERR_CUDA, "met broadcast over %zu GPUs: %s", devs.size(), err.c_str());
+    for (int r : reps) {
+      if (r == root) continue;
+      CK(cudaSetDevice(ctxs[r]->device));
+      CK(cudaEventRecord(ctxs[r]->slots[slots[r]].ready, ctxs[r]->copy));
+    }
+    CK(cudaSetDevice(src->device));
+  }
+  // contexts sharing a GPU with a representative: device-local copies
+  for (int i = 0; i < n; ++i) {
+    if (rep_of[i] == i) continue;
+    lt_ctx* d = ctxs[i];
+    lt_ctx* from = ctxs[rep_of[i]];
+    const int fslot = slots[rep_of[i]];
+    CK(cudaSetDevice(d->device));
+    CK(cudaStreamWaitEvent(d->copy, from->slots[fslot].ready, 0));
+    CK(cudaMemcpyAsync(d->slots[slots[i]].rec, from->slots[fslot].rec, bytes, cudaMemcpyDeviceToDevice, d->copy));
+    CK(cudaEventRecord(d->slots[slots[i]].ready, d->copy));
+    CK(cudaStreamWaitEvent(from->copy, d->slots[slots[i]].ready, 0));  // source not refilled early
+  }
+  for (int i = 0; i < n; ++i) {
+    if (i == root) continue;
+    ctxs[i]->slots[slots[i]].t_met = src->slots[sslot].t_met;
+    ctxs[i]->slots[slots[i]].valid = true;
+  }
+  return LT_OK;
+}
+
+int lt_nccl_version(int32_t* version) {
+  std::string err;
+  int v = 0;
+  if (lt_comm::version(&v, &err)) return fail(LT_ERR_STATE, "%s", err.c_str());
+  *version = v;
+  return LT_OK;
+}
+
+int lt_nccl_ranks(int32_t* nranks) {
+  std::string err;
+  *nranks = lt_comm::communicators(&err);
   return LT_OK;
 }
 

@@ -126,20 +126,18 @@ def run_simulation(ctl, ens, mets, num_devices: int = 1, *, fused: bool = True,
         pool.for_each_device_parallel(init, parallel=parallel)
 
         # fused mode: device 0 stages the next snapshot from the host into its
-        # free slot; the other devices replicate it GPU to GPU
-        def prefetch(d):
-            if rest:
-                eng0 = regions[0].image.engine
-                if d == 0:
-                    eng0.prefetch(met=rest[0])
-                else:
-                    regions[d].image.engine.prefetch_from(eng0)
-
+        # free slot (copy stream); ONE met broadcast (NCCL over NVLink, every
+        # device's copy stream) replicates it into the other devices' free
+        # slots while they keep stepping — the paper's met replication
         def prefetch_all():
-            pool.dispatch(0, lambda: prefetch(0)).result()
+            if not rest:
+                return
+            eng0 = regions[0].image.engine
+            pool.dispatch(0, lambda: eng0.prefetch(met=rest[0])).result()
             if num_devices > 1:
-                for d in range(1, num_devices):
-                    pool.dispatch(d, lambda d=d: prefetch(d)).result()
+                timed("MET_BROADCAST", "MEMORY", device_scope(0),
+                      lambda: eng.Engine.broadcast_staged(
+                          eng0, [regions[d].image.engine for d in range(1, num_devices)]))
         if fused:
             prefetch_all()
 

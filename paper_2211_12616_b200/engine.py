@@ -151,6 +151,23 @@ class Engine:
         self.ctx.copy_slot_from(other.ctx, other._staged, free)
         self._staged = free
 
+    @staticmethod
+    def broadcast_staged(root: "Engine", others) -> None:
+        """Stage `root`'s prefetched snapshot on every engine in `others` by
+        ONE met broadcast (lt_met_broadcast: an NCCL broadcast group over
+        NVLink/NVSwitch, each GPU's copy stream; the paper's met replication)
+        instead of one host upload per GPU."""
+        if root._staged is None:
+            raise RuntimeError("broadcast_staged() from an engine without a staged snapshot")
+        others = [e for e in others if e is not root]
+        if not others:
+            return
+        frees = [min({0, 1, 2} - set(e._met_slots)) for e in others]
+        from .context import met_broadcast
+        met_broadcast([root.ctx] + [e.ctx for e in others], 0, [root._staged] + frees)
+        for e, f in zip(others, frees):
+            e._staged = f
+
     def rotate(self) -> None:
         """met0 <- met1, met1 <- staged (driver_cli.py:139-145)."""
         if self._staged is None:

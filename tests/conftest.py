@@ -125,4 +125,46 @@ def golden_sbr():
     return load_golden("sbr")
 
 
+def hires_met_pair(g):
+    """The 0.25 deg x 137-level window of hires.npz: met rebuilt from the
+    stored axes by tests/golden/hires_met.py (the fields are too large to
+    commit), checked byte for byte against the digest of the fields the
+    reference ran on."""
+    sys.path.insert(0, str(GOLDEN))
+    import hires_met as hm
+    lons, lats, levs = g["lons"], g["lats"], g["levs"]
+    snaps = []
+    for t, phase, dig in ((0.0, 0.0, "digest0"), (10800.0, 5.0, "digest1")):
+        f = hm.fields(lons, lats, levs, phase)
+        assert hm.fields_digest(f) == str(g[dig]), "hires met rebuilt differently"
+        snaps.append(orc.Snapshot(t, lons, lats, levs, f["u"], f["v"], f["w"], f["T"]))
+    return snaps
+
+
+def golden_module_set(name):
+    """(golden dict, Control, met0, met1) of a module-pairs fixture:
+    "modules" (10 x 5 deg x 20, modules.npz) or "hires" (the headline
+    0.25 deg x 137-level shape, hires.npz; keys under "mod_")."""
+    if name == "modules":
+        g = load_golden("modules")
+        return g, modules_ctl(), snapshot_from(g, "m0"), snapshot_from(g, "m1")
+    h = load_golden("hires")
+    g = {k[4:]: v for k, v in h.items() if k.startswith("mod_")}
+    m0, m1 = hires_met_pair(h)
+    return g, modules_ctl(), m0, m1
+
+
+def hires_chain_ctl():
+    """The Control of make_golden.gen_hires's 20-step production chain."""
+    return control(np_max=10**6, t_stop=86400.0, dt_model=180.0, met_dt=10800.0,
+                   turb_dx=50.0, turb_dz=0.1, turb_meso=0.16, rng_mode="counter",
+                   rng_seed_global=2211)
+
+
+@pytest.fixture(scope="session")
+def golden_hires():
+    g = load_golden("hires")
+    return g, hires_met_pair(g)
+
+
 os.environ.setdefault("PYTHONDONTWRITEBYTECODE", "1")

@@ -311,8 +311,9 @@ def gen_chain():
 
 
 def gen_sbr():
-    """cfg1 at reduced N: solid-body rotation on 1 deg x 60 levels, 480
-    steps of advection + position; only the 1-D u(lat) profile is stored."""
+    """cfg1 in full: 1e5 particles, solid-body rotation on 1 deg x 60 levels,
+    480 steps of advection + position (about 5 min on one core); only the
+    1-D u(lat) profile is stored, and only the rows that change."""
     omega = 2.0 * np.pi / 86400.0
     lons, lats, levs = grid(1.0, 1.0, np.geomspace(1013.25, 1.0, 60))
     ulat = f32(omega * 6371000.0 * np.cos(np.deg2rad(lats)))
@@ -324,14 +325,16 @@ def gen_sbr():
     m0, m1 = mk(0.0), mk(86400.0)
     ctl = Control(np_max=10**6, t_stop=86400.0, dt_model=180.0)
     rs = np.random.default_rng(12616)
-    n = 10000
+    n = 100_000
     ens = ensemble_allocate(ctl, n)
     ens.lon[:] = f32(rs.uniform(-180, 180, n))
     ens.lat[:] = f32(rs.uniform(-80, 80, n))
     ens.p[:] = f32(rs.uniform(300, 900, n))
-    init = ens_arrays("init", ens)
+    keep = ("time", "p", "lon", "lat")
+    init = {f"init_{k}": getattr(ens, k).copy() for k in keep}
     run_chain(ctl, ens, m0, m1, None, 480, ("advection", "position"), nd=1)
-    np.savez_compressed(OUT / "sbr.npz", **init, **ens_arrays("final", ens),
+    np.savez_compressed(OUT / "sbr.npz", **init,
+                        **{f"final_{k}": getattr(ens, k).copy() for k in keep},
                         lons=lons, lats=lats, levs=levs, ulat=ulat)
 
 

@@ -47,6 +47,16 @@ def test_ctypes_prototypes_cover_the_header(lib):
     assert set(declared_functions()) == set(_capi.EXPORTED)
 
 
+def test_nccl_resolves_at_run_time(lib):
+    """The met broadcast's NCCL is dlopen'ed (no link-time dependency): the
+    library finds a libnccl here too and reports its version; no
+    communicator exists before a broadcast."""
+    from paper_2211_12616_b200.context import nccl_info
+    info = nccl_info()
+    assert info["version"] is not None and info["version"] >= 22700
+    assert info["ranks"] == 0
+
+
 def test_abi_version_and_no_gpu_paths(lib):
     assert lib.lt_abi_version() == 1
     n = C.c_int32(-1)

@@ -10,7 +10,7 @@ SIMD libm, ~1 ulp apart) are held to 1e-12 relative per call."""
 import numpy as np
 import pytest
 
-from conftest import chain_ctl, control, modules_ctl, snapshot_from
+from conftest import chain_ctl, control, golden_module_set, snapshot_from
 from oracle import lagtrans_oracle as orc
 
 pytestmark = pytest.mark.gpu
@@ -76,10 +76,11 @@ def test_interpolate_met_f64_store(b200, golden_interp):
 
 # ------------------------------------------------------------ module stages
 
-@pytest.fixture(scope="module")
-def mods(golden_modules):
-    g = golden_modules
-    return g, modules_ctl(), snapshot_from(g, "m0"), snapshot_from(g, "m1")
+@pytest.fixture(scope="module", params=["modules", "hires"])
+def mods(request):
+    """Every module on the 10 x 5 deg x 20 fixture and on the headline
+    0.25 deg x 137-level window (hires.npz, levels down to 0.01 hPa)."""
+    return golden_module_set(request.param)
 
 
 def _batch(rng, g):

@@ -197,6 +197,83 @@ def test_met_replication_between_devices(rt):
         assert len(seen) == 2
 
 
+def test_met_broadcast_replicates_slot(rt):
+    """lt_met_broadcast: the root's packed slot lands in each other
+    context's chosen slot (here all contexts share GPU 0, so the transfer is
+    the device-local leg; distinct GPUs take one NCCL broadcast group), with
+    the time level, in stream order after the root's upload; values equal a
+    direct upload's.  Argument errors map onto the reference's exceptions."""
+    _, _, _, ms, syn = rt
+    from paper_2211_12616_b200 import _capi as capi
+    from paper_2211_12616_b200.context import DeviceContext, met_broadcast
+    m0, m1 = syn.analytic_pair(dlon=10.0, dlat=5.0, nlev=16, t0=0.0, t1=3600.0)
+    a, b, c, ref = (DeviceContext(0) for _ in range(4))
+    for x in (a, b, c, ref):
+        x.set_grid(m0.lons, m0.lats, m0.levs)
+    a.load_met(0, m0, key="k0")
+    a.load_met(2, m1, key="k1")
+    ref.load_met(0, m0)
+    ref.load_met(1, m1)
+    met_broadcast([b, a, c], 1, [1, 0, 2])      # root a: slot 0 -> b slot 1, c slot 2
+    met_broadcast([a, b, c], 0, [2, 0, 1])      # slot 2 (m1) -> b slot 0, c slot 1
+    assert b.slot_key(1) == "k0" and c.slot_key(1) == "k1"
+    b.use_met(1, 0)
+    c.use_met(2, 1)
+    ref.use_met(0, 1)
+    rs = np.random.default_rng(4)
+    lon, lat, p = rs.uniform(-180, 180, 4000), rs.uniform(-90, 90, 4000), rs.uniform(5, 1000, 4000)
+    want = ref.interpolate(1234.0, lon, lat, p)
+    np.testing.assert_array_equal(b.interpolate(1234.0, lon, lat, p), want)
+    np.testing.assert_array_equal(c.interpolate(1234.0, lon, lat, p), want)
+    import ctypes as C
+    t = C.c_double()
+    capi.check(b.lib.lt_met_slot_time(b.h, 0, C.byref(t)))
+    assert t.value == 3600.0
+    with pytest.raises(ValueError):
+        met_broadcast([a, b], 0, [2, 3])             # slot out of range
+    with pytest.raises(ValueError):
+        met_broadcast([a, a], 0, [2, 1])             # context twice
+    with pytest.raises(capi.LifecycleError):
+        met_broadcast([a, b], 0, [1, 0])             # root slot never loaded
+    d = DeviceContext(0)
+    d.set_grid(m0.lons[:-2], m0.lats, m0.levs)
+    with pytest.raises(ValueError):
+        met_broadcast([a, d], 0, [0, 0])             # grid differs
+    for x in (a, b, c, ref, d):
+        x.close()
+
+
+def test_driver_rotations_broadcast_met(rt):
+    """driver.run_simulation (fused) on 3 devices with hourly snapshots: each
+    rotation's next snapshot is uploaded once and broadcast (MET_BROADCAST
+    timer rows), and the result equals the one-device run bit for bit."""
+    _, driver, engine, ms, syn = rt
+    lons, lats, levs = syn.grid(10.0, 5.0, 16)
+    mets = [syn.snapshot(3600.0 * k, lons, lats, levs,
+                         syn.era5_like(lons, lats, levs, 7.0 * k, periodic=True))
+            for k in range(4)]
+    ctl = ms.Control(t_stop=3 * 3600.0, dt_model=600.0, met_dt=3600.0, rng_mode="counter",
+                     rng_seed_global=7, output_dt=1e9)
+
+    class Rec:
+        def __init__(self):
+            self.rows = []
+
+        def record(self, name, group, scope, ns):
+            self.rows.append((name, group, scope))
+    outs = []
+    for nd in (1, 3):
+        ens = syn.particles(5000, seed=8)
+        timers = Rec()
+        status, cache = driver.run_simulation(ctl, ens, mets, num_devices=nd, fused=True,
+                                              timers=timers, sort_every=4)
+        assert status == 0
+        outs.append(np.stack([ens.lon, ens.lat, ens.p, ens.time, *cache.uvwp]))
+        n_bc = sum(1 for r in timers.rows if r[0] == "MET_BROADCAST")
+        assert n_bc == (0 if nd == 1 else 2)   # snapshots 2 and 3 are prefetched + broadcast
+    np.testing.assert_array_equal(outs[1], outs[0])
+
+
 def test_faithful_rng_fused_equals_module_path_with_sorts(rt, golden_chain):
     """Faithful mode (the reference default, rng.py:105-126): per-device
     streams seeded rank + 83*device, draws indexed by position in the

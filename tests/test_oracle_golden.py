@@ -9,7 +9,8 @@ the one that generated the fixtures."""
 import numpy as np
 import pytest
 
-from conftest import chain_ctl, control, load_golden, modules_ctl, snapshot_from
+from conftest import (chain_ctl, control, golden_module_set, hires_chain_ctl, load_golden,
+                      snapshot_from)
 from oracle import lagtrans_oracle as orc
 
 TRANS = dict(rtol=1e-13, atol=1e-300)
@@ -108,10 +109,11 @@ def _state(g, tag):
             if f"{tag}_{k}" in g}
 
 
-@pytest.fixture(scope="module")
-def mods(golden_modules):
-    g = golden_modules
-    return g, modules_ctl(), snapshot_from(g, "m0"), snapshot_from(g, "m1")
+@pytest.fixture(scope="module", params=["modules", "hires"])
+def mods(request):
+    """Every stage on the 10 x 5 deg x 20 fixture and on the headline
+    0.25 deg x 137-level window (levels down to 0.01 hPa)."""
+    return golden_module_set(request.param)
 
 
 def test_stage_timesteps(mods):
@@ -169,7 +171,7 @@ def test_stage_sedi(mods):
     np.testing.assert_allclose(p, g["sedi_p"], **TRANS)
 
 
-def test_stage_isosurf_theta(mods, golden_modules):
+def test_stage_isosurf_theta(mods):
     g, ctl, m0, m1 = mods
     s = _state(g, "preiso")
     p, bad = orc.isosurface_pull(ctl, m0, m1, s["lon"], s["lat"], s["p"], s["time"], s["iso"])
@@ -232,9 +234,23 @@ def test_chain_50_steps_all_physics(golden_chain):
     exact(st["time"], g["final_time"])
 
 
-@pytest.mark.slow
+def test_hires_chain_20_steps(golden_hires):
+    """The production chain (advection + turbulent + mesoscale diffusion +
+    position, counter draws) for 20 steps on the 0.25 deg x 137 window."""
+    g, (m0, m1) = golden_hires
+    st = _run_chain(hires_chain_ctl(), {k[6:]: v for k, v in g.items() if k.startswith("chain_")},
+                    m0, m1, 20, ("advection", "turb", "meso", "position"), parts=2)
+    for k in ("lon", "lat", "p"):
+        np.testing.assert_allclose(st[k], g[f"chain_final_{k}"], rtol=1e-11, atol=1e-9)
+    exact(st["time"], g["chain_final_time"])
+    np.testing.assert_allclose(st["uvwp"], g["chain_final_uvwp"], rtol=1e-11, atol=1e-12)
+
+
 def test_sbr_cfg1_shape(golden_sbr):
-    g = golden_sbr
+    """The first 5000 of the fixture's 1e5 cfg1 particles (particles are
+    independent, so a subsample of the reference's full run pins the oracle
+    within seconds)."""
+    g = {k: (v[:5000] if k.startswith(("init_", "final_")) else v) for k, v in golden_sbr.items()}
     lons, lats, levs = g["lons"], g["lats"], g["levs"]
     shape = (lons.size, lats.size, levs.size)
     u = np.broadcast_to(g["ulat"][None, :, None], shape).copy()
@@ -242,6 +258,7 @@ def test_sbr_cfg1_shape(golden_sbr):
     mk = lambda t: orc.close_longitudes(orc.Snapshot(t, lons, lats, levs, u, z, z, np.full(shape, 250.0)))
     m0, m1 = mk(0.0), mk(86400.0)
     ctl = control(t_stop=86400.0, dt_model=180.0)
+    g["init_q"] = np.zeros((5, 5000))
     st = _run_chain(ctl, g, m0, m1, 480, ("advection", "position"), parts=1)
     for k in ("lon", "lat", "p", "time"):
         np.testing.assert_allclose(st[k], g[f"final_{k}"], rtol=1e-12, atol=1e-9)
