@@ -64,6 +64,9 @@ extern "C" {
 #define LT_RUN_RNG_INKERNEL (1u << 0) /* draw randoms in-kernel (else read the batch) */
 #define LT_RUN_DT_ARRAY     (1u << 1) /* read dt from the dt array (else inline)       */
 #define LT_RUN_WRITE_DT     (1u << 2) /* store dt computed by TIMESTEPS               */
+#define LT_RUN_MODULE_CLOCKS (1u << 3) /* fused launch charges SM cycles per module (generic
+                                          kernel; read with lt_module_cycles) — the PHYSICS
+                                          timer rows of driver_cli.py:151-183 / timers.py */
 
 /* rng modes (model_state.py:15 plus the fast Philox mode) */
 #define LT_RNG_FAITHFUL 0
@@ -217,6 +220,13 @@ int lt_run_host_steps(lt_ctx *ctx, const lt_control *ctl, uint32_t modules, int6
    store has ids (a shard or a sorted layout), else by the slot index */
 int lt_rng_fill(lt_ctx *ctx, int32_t mode, uint64_t seed_or_state, int64_t step,
                 int64_t start, int64_t end);
+/* the in-kernel Philox4x32-10 block function (the north star's counter-based
+   generator; words of particle gid at step s are blocks (gid lo, gid hi, s,
+   0|1) under key (seed lo, seed hi)) on n explicit host (ctr[4], key[2])
+   pairs, run on the device: out = n x 4 words.  A known-answer hook:
+   Random123's kat_vectors must come back bit for bit. */
+int lt_philox4x32_10(lt_ctx *ctx, int32_t n, const uint32_t *ctr, const uint32_t *key,
+                     uint32_t *out);
 /* interpolate_met (physics.py:69-79) at n host points: out = u,v,w,T rows (4n) */
 int lt_interpolate(lt_ctx *ctx, int64_t n, const double *t, const double *lon,
                    const double *lat, const double *p, double *out);
@@ -277,6 +287,14 @@ int lt_write_atm(const char *path, int64_t n, int32_t nq, const double *time, co
                  const double *zeta, const double *lon, const double *lat, const double *q,
                  int64_t q_stride, int32_t threads);
 int lt_format_double(double x, char *out, int32_t cap, int32_t *len);
+
+/* SM cycles the LT_RUN_MODULE_CLOCKS launches spent per module, summed
+   over particles, in the order timesteps, random draws, advection, turb,
+   meso, convection, sedi, decay, isosurf, position, meteo, isosurf_init;
+   shares of a launch's event time give the reference's per-module
+   PHYSICS timer rows for a fused step (timers.py:40-54) */
+#define LT_N_MODULE_CLOCKS 12
+int lt_module_cycles(lt_ctx *ctx, uint64_t *cycles, int32_t reset);
 
 /* event timing of the last lt_run / lt_sort_by_box on this context */
 int lt_timing(lt_ctx *ctx, int32_t enable);

@@ -34,6 +34,12 @@ MOD_ISOSURF_INIT = 1 << 10
 RUN_RNG_INKERNEL = 1 << 0
 RUN_DT_ARRAY = 1 << 1
 RUN_WRITE_DT = 1 << 2
+RUN_MODULE_CLOCKS = 1 << 3
+# lt_module_cycles slots -> the reference's PHYSICS timer names (driver_cli.py:151-183)
+MODULE_CLOCK_NAMES = ("module_timesteps", "generate_random_nums", "module_advection",
+                      "module_diffusion_turb", "module_diffusion_meso", "module_convection",
+                      "module_sedi", "module_decay", "module_isosurf", "module_position",
+                      "module_meteo", "module_isosurf_init")
 
 RNG_MODES = {"faithful": 0, "counter": 1, "philox": 2}
 ISO_MODES = {"off": 0, "pressure": 1, "theta": 2}
@@ -124,6 +130,8 @@ _PROTOS = {
     "lt_run": ([_P, C.POINTER(LtControl), _U32, _I64, _I64, _I64, _U64, _I64, _U32], C.c_int),
     "lt_run_steps": ([_P, C.POINTER(LtControl), _U32, _I64, _I64, _I64, _I32, _U32], C.c_int),
     "lt_rng_fill": ([_P, _I32, _U64, _I64, _I64, _I64], C.c_int),
+    "lt_philox4x32_10": ([_P, _I32, _P, _P, _P], C.c_int),
+    "lt_module_cycles": ([_P, _P, _I32], C.c_int),
     "lt_iso_counter": ([_P, C.POINTER(_I64), _I32], C.c_int),
     "lt_sort_by_box": ([_P, _I64, _I64], C.c_int),
     "lt_set_home_rows": ([_P, _U32], C.c_int),
@@ -160,7 +168,10 @@ def load(path: Path | None = None):
             "(python -m paper_2211_12616_b200._build or __graft_entry__.build()); "
             "there is no CPU fallback")
     lib = C.CDLL(str(path))
-    for name, (args, res) in _PROTOS.items():
+    variant = "LAGTRANS_B200_LIB" in os.environ   # an A/B build (tools/ab.sh) may predate
+    for name, (args, res) in _PROTOS.items():      # newer entry points; the in-tree one may not
+        if variant and not hasattr(lib, name):
+            continue
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res

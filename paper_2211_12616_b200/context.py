@@ -353,6 +353,13 @@ class DeviceContext:
     def timing(self, on: bool) -> None:
         capi.check(self.lib.lt_timing(self.h, int(on)))
 
+    def module_cycles(self, reset: bool = True) -> np.ndarray:
+        """SM cycles per module of the RUN_MODULE_CLOCKS launches so far
+        (slots in capi.MODULE_CLOCK_NAMES order)."""
+        out = np.zeros(len(capi.MODULE_CLOCK_NAMES), dtype=np.uint64)
+        capi.check(self.lib.lt_module_cycles(self.h, capi.ptr(out), int(reset)))
+        return out
+
     def last_elapsed_ms(self) -> float:
         v = C.c_float()
         capi.check(self.lib.lt_last_elapsed_ms(self.h, C.byref(v)))

@@ -43,6 +43,7 @@ int fail(int code, const char* fmt, ...) {
 
 struct AxisHost {
   double* dev = nullptr;
+  double* rinv = nullptr;  // per cell RN(1 / (x[i+1] - x[i])) (exact path: Markstein quotient)
   double2* cell = nullptr;  // per cell {x[i], fp32 1/(x[i+1]-x[i]) in the low word}
   double lo = 0.0, hi = 0.0;
   int n = 0;
@@ -93,7 +94,7 @@ struct lt_ctx {
   uint32_t* sort_buf = nullptr;  // 4 * cap (keys in/out, vals in/out)
   void* cub_temp = nullptr;
   size_t cub_bytes = 0;
-  unsigned long long* counters = nullptr;  // [0] iso_nonconverged
+  unsigned long long* counters = nullptr;  // [0] iso_nonconverged, [8, 8 + CK_N) module cycles
   int* bad = nullptr;
 
   // met
@@ -157,8 +158,10 @@ int upload_axis(AxisHost& ax, const double* x, int n, cudaStream_t st) {
   if (ax.dev && ax.n != n) {
     cudaFree(ax.dev);
     cudaFree(ax.cell);
+    cudaFree(ax.rinv);
     ax.dev = nullptr;
     ax.cell = nullptr;
+    ax.rinv = nullptr;
   }
   ax.n = n;
   if (!ax.dev) {
@@ -166,7 +169,15 @@ int upload_axis(AxisHost& ax, const double* x, int n, cudaStream_t st) {
     if (rc) return rc;
     rc = alloc_dev(reinterpret_cast<void**>(&ax.cell), sizeof(double2) * n, "axis cells");
     if (rc) return rc;
+    rc = alloc_dev(reinterpret_cast<void**>(&ax.rinv), sizeof(double) * n, "axis reciprocals");
+    if (rc) return rc;
   }
+  // correctly rounded reciprocal cell widths: with them the exact kernels'
+  // fraction (x - x[i]) / (x[i+1] - x[i]) is one multiply and two FMAs and
+  // still the correctly rounded quotient numpy computes (lt_device.cuh div_cr)
+  std::vector<double> rinv(n, 0.0);
+  for (int i = 0; i + 1 < n; ++i) rinv[i] = 1.0 / (x[i + 1] - x[i]);
+  CK(cudaMemcpyAsync(ax.rinv, rinv.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
   std::vector<double2> cell(n);
   for (int i = 0; i < n; ++i) {
     const float r = i + 1 < n ? static_cast<float>(1.0 / (x[i + 1] - x[i])) : 0.0f;
@@ -186,6 +197,7 @@ Axis view(const AxisHost& a) {
   Axis v;
   v.x = a.dev;
   v.cell = a.cell;
+  v.rinv = a.rinv;
   v.lo = a.lo;
   v.hi = a.hi;
   v.n = a.n;
@@ -330,11 +342,11 @@ static int ctx_init(lt_ctx* c) {
   CK(cudaEventCreateWithFlags(&c->staging_free, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->compute_mark, cudaEventDisableTiming));
   for (auto& s : c->slots) CK(cudaEventCreateWithFlags(&s.ready, cudaEventDisableTiming));
-  int rc = alloc_dev(reinterpret_cast<void**>(&c->counters), 8 * sizeof(unsigned long long), "counters");
+  int rc = alloc_dev(reinterpret_cast<void**>(&c->counters), 32 * sizeof(unsigned long long), "counters");
   if (rc) return rc;
   rc = alloc_dev(reinterpret_cast<void**>(&c->bad), sizeof(int), "flag");
   if (rc) return rc;
-  CK(cudaMemsetAsync(c->counters, 0, 8 * sizeof(unsigned long long), c->stream));
+  CK(cudaMemsetAsync(c->counters, 0, 32 * sizeof(unsigned long long), c->stream));
   CK(cudaMemsetAsync(c->bad, 0, sizeof(int), c->stream));
   CK(cudaStreamSynchronize(c->stream));
   return LT_OK;
@@ -371,6 +383,7 @@ int lt_ctx_destroy(lt_ctx* c) {
   for (AxisHost* a : {&c->ax_lon, &c->ax_lat, &c->ax_lev, &c->cl_lat, &c->cl_p}) {
     free_dev(a->dev);
     free_dev(a->cell);
+    free_dev(a->rinv);
   }
   free_dev(c->hno3);
   free_dev(c->p_trop);
@@ -905,6 +918,7 @@ static int run_typed(lt_ctx* c, const lt_control* ctl, uint32_t modules, int64_t
   a.modules = modules; a.flags = flags; a.step = step; a.nsteps = nsteps;
   a.faithful_state = fstate; a.faithful_base = fbase;
   a.iso_nonconv = c->counters;
+  a.mod_cycles = c->counters + 8;
   static_assert(sizeof(lt_control) == sizeof(Control), "control layout");
   std::memcpy(&a.ctl, ctl, sizeof(Control));
   {
@@ -1173,6 +1187,41 @@ int lt_rng_fill(lt_ctx* c, int32_t mode, uint64_t seed, int64_t step, int64_t st
   if (c->timing) CK(cudaEventRecord(c->ev_start, c->stream));
   CK(launch_rng_fill(mode, seed, step, start, end, c->ids, c->rnd_conv, c->rnd_turb, c->rnd_meso, c->stream));
   if (c->timing) { CK(cudaEventRecord(c->ev_stop, c->stream)); c->timed_once = true; }
+  return LT_OK;
+}
+
+int lt_module_cycles(lt_ctx* c, uint64_t* cycles, int32_t reset) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  static_assert(CK_N <= LT_N_MODULE_CLOCKS, "clock slots");
+  unsigned long long v[LT_N_MODULE_CLOCKS] = {};
+  CK(cudaMemcpyAsync(v, c->counters + 8, sizeof(unsigned long long) * CK_N, cudaMemcpyDeviceToHost,
+                     c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (reset) CK(cudaMemsetAsync(c->counters + 8, 0, sizeof(unsigned long long) * CK_N, c->stream));
+  for (int k = 0; k < LT_N_MODULE_CLOCKS; ++k) cycles[k] = v[k];
+  return LT_OK;
+}
+
+int lt_philox4x32_10(lt_ctx* c, int32_t n, const uint32_t* ctr, const uint32_t* key, uint32_t* out) {
+  int rc = check_ctx(c);
+  if (rc) return rc;
+  if (n < 0) return fail(LT_ERR_ARG, "negative block count");
+  if (n == 0) return LT_OK;
+  void* d = nullptr;
+  // counters (16 B each), keys (8 B), outputs (16 B): each array 16-byte aligned
+  const size_t b_ctr = 16 * static_cast<size_t>(n), b_key = (8 * static_cast<size_t>(n) + 15) & ~size_t(15);
+  if ((rc = alloc_dev(&d, 2 * b_ctr + b_key, "philox kat"))) return rc;
+  char* base = static_cast<char*>(d);
+  cudaError_t e = cudaMemcpyAsync(base, ctr, b_ctr, cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(base + b_ctr, key, b_key, cudaMemcpyHostToDevice, c->stream);
+  if (e == cudaSuccess)
+    e = launch_philox_kat(reinterpret_cast<uint32_t*>(base), reinterpret_cast<uint32_t*>(base + b_ctr),
+                          reinterpret_cast<uint32_t*>(base + b_ctr + b_key), n, c->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out, base + b_ctr + b_key, b_ctr, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  free_dev(d);
+  CK(e);
   return LT_OK;
 }
 

@@ -224,6 +224,22 @@ cudaError_t launch_rng_fill(int mode, uint64_t seed, int64_t step, int64_t start
   return cudaGetLastError();
 }
 
+// the in-kernel generator's block function on explicit (counter, key)
+// pairs: the known-answer hook for Philox4x32-10 (Random123's kat_vectors)
+__global__ void philox_kat_kernel(const uint4* ctr, const uint2* key, uint4* out, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = philox(ctr[i], key[i]);
+}
+
+cudaError_t launch_philox_kat(const uint32_t* ctr, const uint32_t* key, uint32_t* out, int n,
+                              cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  philox_kat_kernel<<<(n + 127) / 128, 128, 0, st>>>(reinterpret_cast<const uint4*>(ctr),
+                                                     reinterpret_cast<const uint2*>(key),
+                                                     reinterpret_cast<uint4*>(out), n);
+  return cudaGetLastError();
+}
+
 template <class Rec>
 cudaError_t launch_box_keys(const MetView<Rec>& m, const double* lon, const double* lat,
                             const double* p, int64_t start, int64_t n, uint32_t* keys,

@@ -82,6 +82,8 @@ cudaError_t launch_sample(const MetView<Rec>& m, const double* t, const double* 
 template <class Rec>
 cudaError_t launch_locate(const MetView<Rec>& m, int fast, const double* lon, const double* lat,
                           const double* p, int32_t* out, int64_t n, cudaStream_t st);
+cudaError_t launch_philox_kat(const uint32_t* ctr, const uint32_t* key, uint32_t* out, int n,
+                              cudaStream_t st);
 cudaError_t launch_iota(uint32_t* ids, int64_t offset, int64_t count, int64_t first,
                         cudaStream_t st);
 cudaError_t launch_fill(double* x, int64_t n, double v, cudaStream_t st);

@@ -37,6 +37,9 @@ static cudaError_t launch_fixed(const StepArgs<Rec>& a, cudaStream_t st) {
 
 template <class Rec, int FAST>
 static cudaError_t launch_prec(const StepArgs<Rec>& a, cudaStream_t st) {
+  // per-module cycle attribution runs in the generic kernel (the
+  // specialised ones carry no instrumentation)
+  if (a.flags & F_MODULE_CLOCKS) return launch_fixed<Rec, 0, FAST, -1>(a, st);
   // the production chain gets its in-kernel generator fixed at compile time;
   // with a pending box-sort permutation it applies it on the fly
   if (a.perm) {
@@ -75,7 +78,7 @@ static cudaError_t launch_prec(const StepArgs<Rec>& a, cudaStream_t st) {
 // production chain (it reads and writes every hot row) with a compile-time
 // in-kernel generator
 bool perm_capable(uint32_t modules, uint32_t flags, int rng_mode) {
-  return modules == kChainAdvDiff && (flags & F_RNG_INKERNEL) &&
+  return modules == kChainAdvDiff && (flags & F_RNG_INKERNEL) && !(flags & F_MODULE_CLOCKS) &&
          (rng_mode == RNG_COUNTER || rng_mode == RNG_PHILOX || rng_mode == RNG_FAITHFUL);
 }
 

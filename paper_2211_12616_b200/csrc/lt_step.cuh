@@ -60,6 +60,7 @@ struct StepArgs {
   uint64_t faithful_state;
   int64_t faithful_base;
   unsigned long long* iso_nonconv;
+  unsigned long long* mod_cycles;  // CK_N counters (F_MODULE_CLOCKS launches)
   Control ctl;
   StepConst kc;
   MetView<Rec> met;
@@ -116,9 +117,10 @@ struct Ops {
   // physics.py:206-222 (module_sedi): Stokes settling hop of p
   __device__ static double sedi_hop(const Control& ctl, double p, double temp, double dt) {
     const double rho = 100.0 * p / (kRAir * temp);
-    const double vs = 2.0 * (ctl.sedi_radius * ctl.sedi_radius) * (ctl.sedi_density - rho) *
-                      kG0 / (9.0 * kEtaAir);
-    return p + (rho * kG0 * vs * dt) / 100.0;
+    constexpr double k9eta = 9.0 * kEtaAir;
+    const double vs = div_cr(2.0 * (ctl.sedi_radius * ctl.sedi_radius) * (ctl.sedi_density - rho) *
+                             kG0, k9eta, 1.0 / k9eta);
+    return p + div_cr(rho * kG0 * vs * dt, 100.0, 0.01);
   }
   // physics.py:238-264 (module_isosurf, theta): up to 10 fixed-point steps
   // p <- 1000 (T(p) / theta0)^(1/kappa) while |dp| >= 0.1; false if still pending
@@ -138,7 +140,7 @@ struct Ops {
   // physics.py turb vertical hop: p - rho g dz / 100 with rho = 100 p / (R T)
   __device__ static double vertical_hop(double p, double temp, double dz) {
     const double rho = 100.0 * p / (kRAir * temp);
-    return p + (-(rho * kG0 * dz) / 100.0);
+    return p + div_cr(-(rho * kG0 * dz), 100.0, 0.01);
   }
   __device__ static uint32_t cell(const MetView<Rec>& m, double lon, double lat, double p) {
     return cell_of(m, lon, lat, p).r00;
@@ -333,6 +335,26 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
   unsigned long long nonconv = 0;
 
   // per-launch switches, decided once outside the particle loop
+  // F_MODULE_CLOCKS (generic kernels only; the specialised ones compile it
+  // out): SM cycles between module boundaries are charged to the module
+  // that ends there (draws to CK_RNG), summed over threads — the per-module
+  // split of a fused launch behind the reference's PHYSICS timer rows
+  const bool clocks = FIXED == 0 && (a.flags & F_MODULE_CLOCKS);
+  unsigned long long cyc[CK_N];
+  long long t_last = 0;
+  if (FIXED == 0) {
+#pragma unroll
+    for (int k = 0; k < CK_N; ++k) cyc[k] = 0;
+  }
+#define LT_CLOCK(slot)                                  \
+  do {                                                  \
+    if (FIXED == 0 && clocks) {                         \
+      const long long t_ = clock64();                   \
+      cyc[slot] += static_cast<unsigned long long>(t_ - t_last); \
+      t_last = t_;                                      \
+    }                                                   \
+  } while (0)
+
   const bool want_turb = (mods & M_TURB) && (ctl.turb_dx != 0.0 || ctl.turb_dz != 0.0);
   const bool want_meso = (mods & M_MESO) && ctl.turb_meso != 0.0;
   const bool want_conv = (mods & M_CONVECTION) && ctl.conv_prob != 0.0;
@@ -362,6 +384,7 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
       prefetch_l2(a.ids + nx);
     }
 #endif
+    if (FIXED == 0 && clocks) t_last = clock64();
     double time = ld_state(a.time + src), lon = ld_state(a.lon + src), lat = ld_state(a.lat + src),
            p = ld_state(a.p + src);
 
@@ -391,6 +414,7 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
       }
       const bool act = dt > 0.0;
       if (PERM) meso_wrote = want_meso && act;
+      LT_CLOCK(CK_TIMESTEPS);
 
 #ifndef LT_LATE_DRAWS
       // fast path with a compile-time generator: the six normals are pure ALU
@@ -428,6 +452,7 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
           O::sample(a.met, time, lon, lat, p, 8, v);
           a.iso_var[row_index(a, s, src, HOME_ISO)] = v[3] * O::power(1000.0 / p, kKappa);
         }
+        LT_CLOCK(CK_ISOSURF_INIT);
       }
 
       // physics.py:91-116 (module_advection): explicit midpoint.  The two
@@ -445,6 +470,7 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
         }
         lon = xs; lat = ys; p = zs;
         time = time + dt;
+        LT_CLOCK(CK_ADVECTION);
       }
 
       constexpr uint32_t kNoColumn = 0xFFFFFFFFu;
@@ -464,6 +490,7 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
 #endif
         if (kBoth) philox_turb_meso(ctl.rng_seed_global, stp, gid, xt, zmeso);
         else draws<O, RM>(a, s, gid, 1, xt, stp);
+        LT_CLOCK(CK_RNG);
         if (turb_h) {
           double sig = a.kc.turb_sx;
           if (__builtin_expect(dt != a.kc.dt, 0)) sig = sqrt(2.0 * ctl.turb_dx * dt);
@@ -479,6 +506,7 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
           const double dz = sz * xt[2];
           p = O::vertical_hop(p, v[3], dz);
         }
+        LT_CLOCK(CK_TURB);
       }
 
       // physics.py:150-188 (module_diffusion_meso): AR(1) with met0 cell spread
@@ -490,6 +518,7 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
 #endif
         if (kBoth && want_turb) { xm[0] = zmeso[0]; xm[1] = zmeso[1]; xm[2] = zmeso[2]; }
         else draws<O, RM>(a, s, gid, 2, xm, stp);
+        LT_CLOCK(CK_RNG);
         // the vertical hop moved only p: the T sample's lon/lat column holds
         const uint32_t r00 = tcol != kNoColumn ? O::cell_in_column(a.met, tcol, p)
                                                : O::cell(a.met, lon, lat, p);
@@ -517,14 +546,17 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
         lat = lat + pert[1] * dt * kDegPerM;
         lon = nlon;
         p = p + pert[2] * dt;
+        LT_CLOCK(CK_MESO);
       }
 
       // physics.py:191-203 (module_convection)
       if (want_conv && act) {
         double xc[3];
         draws<O, RM>(a, s, gid, 0, xc, stp);
+        LT_CLOCK(CK_RNG);
         if (p > ctl.conv_p_top && xc[0] < ctl.conv_prob)
           p = O::conv_target(ctl, a.kc, xc[0]);
+        LT_CLOCK(CK_CONVECTION);
       }
 
       // physics.py:206-222 (module_sedi): Stokes settling
@@ -532,6 +564,7 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
         double v[4];
         O::sample(a.met, time, lon, lat, p, 8, v);
         p = O::sedi_hop(ctl, p, v[3], dt);
+        LT_CLOCK(CK_SEDI);
       }
 
       // decay (new module): q[slot] *= exp(-dt / tau) while active
@@ -539,6 +572,7 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
           ctl.decay_slot < a.nq) {
         double* qs = a.q + static_cast<int64_t>(ctl.decay_slot) * a.cap + row_index(a, s, src, HOME_Q);
         *qs = *qs * (dt == a.kc.dt ? a.kc.decay : exp(-dt / ctl.decay_tau));
+        LT_CLOCK(CK_DECAY);
       }
 
       // physics.py:238-264 (module_isosurf): applies to every particle
@@ -549,6 +583,7 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
           const double theta0 = a.iso_var[row_index(a, s, src, HOME_ISO)];
           nonconv += O::isosurf_theta(a.met, time, lon, lat, p, theta0) ? 0ull : 1ull;
         }
+        LT_CLOCK(CK_ISOSURF);
       }
 
       // physics.py:267-287 (module_position): pole reflection, lon wrap, clamp
@@ -567,6 +602,7 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
           lon = m - 180.0;
         }
         p = np_min(np_max(p, ctl.p_top), ctl.p_surf);
+        LT_CLOCK(CK_POSITION);
       }
 
       // physics.py:290-301 (module_meteo): sample T,u,v and climatology
@@ -579,6 +615,7 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
         a.q[2 * a.cap + qi] = v[1];
         a.q[3 * a.cap + qi] = clim_hno3(a.clim, lat, p);
         a.q[4 * a.cap + qi] = p < clim_ptrop(a.clim, lat) ? 1.0 : 0.0;
+        LT_CLOCK(CK_METEO);
       }
 
     }  // steps
@@ -605,6 +642,16 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
     }
   }
 
+#undef LT_CLOCK
+  if (FIXED == 0 && clocks) {  // warp sums, one atomic per warp and module
+#pragma unroll
+    for (int k = 0; k < CK_N; ++k) {
+      unsigned long long v = cyc[k];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+      if ((threadIdx.x & 31) == 0 && v) atomicAdd(a.mod_cycles + k, v);
+    }
+  }
   if (mods & M_ISOSURF) {
     // warp-aggregated counter (CacheState.iso_nonconverged)
     unsigned long long tot = nonconv;

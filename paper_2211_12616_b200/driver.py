@@ -77,10 +77,17 @@ DEFAULT_SORT_EVERY = 15   # measured optimum at cfg3
 def run_simulation(ctl, ens, mets, num_devices: int = 1, *, fused: bool = True,
                    modules: int | None = None, sort_every: int | None = None, clim=None,
                    timers=None, on_output=None, parallel: bool = True,
-                   device_map=None):
+                   device_map=None, module_timers: bool = False):
     """Advance `ens` (host ParticleEnsemble, updated in place at every
     output time) from ctl.t_start to ctl.t_stop.  Returns (status, cache):
     status 0 on success, 1 when a device task failed (driver_cli.py:196-199).
+
+    module_timers (fused mode): every step is one instrumented fused launch
+    that charges SM cycles to the module that spends them, and the launch's
+    CUDA-event time is split by those shares into the reference's PHYSICS
+    rows (module_timesteps, generate_random_nums, module_advection, ...;
+    driver_cli.py:151-183, test_acceptance.py:284-305).  Off by default:
+    the production steps run the specialised, uninstrumented kernels.
     """
     if sort_every is None:      # box-sort the fused path by default (results never change)
         sort_every = DEFAULT_SORT_EVERY if fused else 0
@@ -172,7 +179,7 @@ def run_simulation(ctl, ens, mets, num_devices: int = 1, *, fused: bool = True,
             # box sort, output) as one multi-step launch (Engine.step_many:
             # identical results, each particle advanced in registers)
             run, t_end = 1, t_next
-            if fused:
+            if fused and not module_timers:
                 while step + run < n_steps:
                     t_more = min(t_end + ctl.dt_model, ctl.t_stop)
                     if (met1.t_met < t_more or (sort_every and (step + run) % sort_every == 0)
@@ -190,11 +197,13 @@ def run_simulation(ctl, ens, mets, num_devices: int = 1, *, fused: bool = True,
                         img.engine.step_many(img.ctl, step, run, modules, device_id=d)
                     else:
                         img.engine.step(img.ctl, step, modules, device_id=d,
-                                        num_devices=num_devices)
+                                        num_devices=num_devices, module_clocks=module_timers)
                     ms = ctx.last_elapsed_ms()
                     ctx.timing(False)
                     timers.record("module_fused_step", "PHYSICS", device_scope(d),
                                   int(ms * 1e6))
+                    if module_timers:
+                        _record_module_split(ctx, modules, ms, timers, device_scope(d))
             else:
                 def device_step(d, step=step, t_next=t_next):
                     _module_step(regions[d].image, ranges[d], d, step, t_next, rng,
@@ -224,6 +233,32 @@ def run_simulation(ctl, ens, mets, num_devices: int = 1, *, fused: bool = True,
                       lambda r=region: pool.region_delete(r))
         pool.shutdown()
     return status, cache
+
+
+_SPLIT_BITS = {"module_timesteps": capi.MOD_TIMESTEPS, "module_advection": capi.MOD_ADVECTION,
+               "module_diffusion_turb": capi.MOD_TURB, "module_diffusion_meso": capi.MOD_MESO,
+               "module_convection": capi.MOD_CONVECTION, "module_sedi": capi.MOD_SEDI,
+               "module_decay": capi.MOD_DECAY, "module_isosurf": capi.MOD_ISOSURF,
+               "module_position": capi.MOD_POSITION, "module_meteo": capi.MOD_METEO}
+
+
+def _record_module_split(ctx, modules, ms, timers, scope):
+    """One instrumented fused launch of `ms` milliseconds: each enabled
+    module's row gets its share of the launch's SM cycles (random draws as
+    generate_random_nums, as the reference times them); modules that are
+    enabled but did no work (e.g. isosurf off in the control) get 0 ns."""
+    cyc = ctx.module_cycles(reset=True).astype(np.float64)
+    total = cyc.sum()
+    for name, c in zip(capi.MODULE_CLOCK_NAMES, cyc):
+        bit = _SPLIT_BITS.get(name)
+        if name == "generate_random_nums":
+            on = bool(modules & (capi.MOD_TURB | capi.MOD_MESO | capi.MOD_CONVECTION))
+        elif name == "module_isosurf_init":
+            on = False
+        else:
+            on = bool(modules & bit)
+        if on:
+            timers.record(name, "PHYSICS", scope, int(ms * 1e6 * (c / total if total else 0.0)))
 
 
 def _module_step(img, work, d, step, t_next, rng, met0, met1, timers):

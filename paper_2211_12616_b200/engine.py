@@ -185,16 +185,19 @@ class Engine:
             self.ctx.run(ctl, capi.MOD_ISOSURF_INIT, 0, self.n)
 
     def step(self, ctl, step: int, modules: int = ADV_DIFF, device_id: int = 0,
-             num_devices: int = 1) -> None:
-        """One fused time step of every particle in the shard."""
+             num_devices: int = 1, module_clocks: bool = False) -> None:
+        """One fused time step of every particle in the shard.  With
+        module_clocks the launch also charges its SM cycles per module
+        (ctx.module_cycles; the generic, instrumented kernel runs)."""
         fstate = 0
         if ctl.rng_mode == "faithful":   # the reference fills a batch every step
             if self.faithful_state is None:
                 self.faithful_state = rng_seed_for(ctl.mpi_rank, device_id)
             fstate = self.faithful_state
             self.faithful_state = advance_faithful(fstate, self.n)
+        flags = capi.RUN_RNG_INKERNEL | (capi.RUN_MODULE_CLOCKS if module_clocks else 0)
         self.ctx.run(ctl, modules, 0, self.n, step=step, faithful_state=fstate,
-                     faithful_base=self.first_id, flags=capi.RUN_RNG_INKERNEL)
+                     faithful_base=self.first_id, flags=flags)
         self._last_modules = modules
 
     def step_many(self, ctl, step: int, nsteps: int, modules: int = ADV_DIFF,

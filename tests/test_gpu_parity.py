@@ -358,3 +358,88 @@ def test_rng_fill_unaffected_by_earlier_id_layouts(b200):
     exact(b.convection[100:900], conv)
     np.testing.assert_allclose(b.diff_turb.reshape(-1, 3)[100:900], turb, rtol=1e-12, atol=1e-12)
     np.testing.assert_allclose(b.diff_meso.reshape(-1, 3)[100:900], meso, rtol=1e-12, atol=1e-12)
+
+
+# ------------------------------------------------------------ generator KATs
+
+# Random123 kat_vectors, philox4x32 10: (ctr[4], key[2]) -> out[4]
+PHILOX_KAT = [
+    ((0x00000000, 0x00000000, 0x00000000, 0x00000000), (0x00000000, 0x00000000),
+     (0x6627e8d5, 0xe169c58d, 0xbc57ac4c, 0x9b00dbd8)),
+    ((0xffffffff, 0xffffffff, 0xffffffff, 0xffffffff), (0xffffffff, 0xffffffff),
+     (0x408f276d, 0x41c83b0e, 0xa20bc7c6, 0x6d5451fd)),
+    ((0x243f6a88, 0x85a308d3, 0x13198a2e, 0x03707344), (0xa4093822, 0x299f31d0),
+     (0xd16cfe09, 0x94fdcceb, 0x5001e420, 0x24126ea1)),
+]
+
+
+def test_philox_device_known_answers(b200):
+    """The in-kernel Philox4x32-10 block function, run on the device through
+    lt_philox4x32_10, reproduces Random123's known-answer vectors."""
+    import ctypes as C
+    from paper_2211_12616_b200 import _capi as capi
+    from paper_2211_12616_b200.physics import default_context
+    ctx = default_context()
+    ctr = np.array([v[0] for v in PHILOX_KAT], dtype=np.uint32)
+    key = np.array([v[1] for v in PHILOX_KAT], dtype=np.uint32)
+    out = np.zeros((len(PHILOX_KAT), 4), dtype=np.uint32)
+    capi.check(ctx.lib.lt_philox4x32_10(ctx.h, len(PHILOX_KAT), capi.ptr(ctr), capi.ptr(key),
+                                        capi.ptr(out)))
+    exact(out, np.array([v[2] for v in PHILOX_KAT], dtype=np.uint32))
+
+
+def test_philox_draws_follow_the_kat_words(b200):
+    """Seed 0, step 0, particle 0 is Philox block (0, 0, 0, 0) under key
+    (0, 0) — KAT vector 1 — so the batch's convection uniform is the 53-bit
+    uniform of its first two words and the first turbulent normal the
+    Box-Muller transform of words 3 and 4 (lt_device.cuh philox_draws)."""
+    _, rng, _ = b200
+    from paper_2211_12616_b200.partition import WorkRange
+    w = PHILOX_KAT[0][2]
+    b = rng.batch_allocate(4)
+    rng.generate_random_nums(rng.RngState("philox", 0), 0, WorkRange(0, 0, 4), 0, b)
+    conv = ((w[0] >> 5) * 67108864.0 + (w[1] >> 6)) / 9007199254740992.0
+    assert b.convection[0] == conv
+    u1 = (w[2] + 0.5) * 2.3283064365386963e-10
+    u2 = (w[3] + 0.5) * 2.3283064365386963e-10
+    z0 = np.sqrt(-2.0 * np.log(u1)) * np.cos(2.0 * np.pi * u2)
+    np.testing.assert_allclose(b.diff_turb[0], z0, rtol=1e-13, atol=1e-15)
+
+
+# ------------------------------------------------------------ met packing
+
+@pytest.mark.parametrize("path", ["fields", "nodes"])
+def test_close_lon_packing_on_device(b200, path):
+    """LT_MET_CLOSE_LON (met_periodic, ingest.py:195-207, done by the
+    packing kernel instead of on the host): a global snapshot WITHOUT its
+    +360 column, loaded with the flag into a closed grid, interpolates bit
+    for bit like the host-closed snapshot — for lt_met_load (separate
+    fields) and lt_met_load_nodes (interleaved float32 nodes, the streaming
+    path of cfg4)."""
+    _, _, ms = b200
+    from paper_2211_12616_b200 import synthetic as syn
+    from paper_2211_12616_b200.context import DeviceContext
+    lons, lats, levs = syn.grid(5.0, 5.0, 24)
+    f = syn.era5_like(lons, lats, levs, 13.0)                    # nx columns, open
+    closed = syn.snapshot(600.0, lons, lats, levs, f, periodic=True)
+    assert closed.lons.size == lons.size + 1
+    ref, got = DeviceContext(0), DeviceContext(0)
+    for c in (ref, got):
+        c.set_grid(closed.lons, closed.lats, closed.levs)
+    ref.load_met(0, closed)
+    if path == "fields":
+        open_met = ms.MeteoField(600.0, lons, lats, levs, f["u"], f["v"], f["w"], f["T"])
+        got.load_met(0, open_met, close_lon=True)
+    else:
+        nodes = np.stack([f["u"], f["v"], f["w"], f["T"]], axis=-1).astype(np.float32)
+        got.load_met_nodes(0, 600.0, np.ascontiguousarray(nodes), close_lon=True)
+    ref.use_met(0, 0)
+    got.use_met(0, 0)
+    rs = np.random.default_rng(3)
+    n = 20000
+    lon = rs.uniform(-181.0, 181.0, n)
+    lon[:200] = rs.uniform(175.0, 180.0, 200)                   # inside the closing column
+    lat, p = rs.uniform(-90, 90, n), rs.uniform(0.5, 1100, n)
+    exact(got.interpolate(600.0, lon, lat, p), ref.interpolate(600.0, lon, lat, p))
+    ref.close()
+    got.close()

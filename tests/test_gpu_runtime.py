@@ -162,6 +162,50 @@ def test_module_mode_timer_contract(rt, golden_chain):
     assert all(ns >= 0 for *_, ns in recs)
 
 
+def test_fused_mode_timer_contract(rt, golden_chain):
+    """The production (fused) path meets the same c10 contract: with
+    module_timers each fused launch charges its SM cycles per module and its
+    CUDA-event time is split into the reference's PHYSICS rows
+    (module_advection ... module_meteo, generate_random_nums), per device;
+    the per-module rows of a step add up to its module_fused_step row, and
+    the instrumented kernel changes no result bit."""
+    _, driver, _, ms, _ = rt
+    g = golden_chain
+    recs = []
+
+    class Sink:
+        def record(self, name, group, scope, ns):
+            recs.append((group, name, scope, ns))
+
+    ctl = _ctl(ms, output_dt=1e9, t_stop=540.0)
+    mets = [snapshot_from(g, "m0"), snapshot_from(g, "m1")]
+    outs = []
+    for module_timers in (True, False):
+        ens = _ens(ms, g, "init")
+        status, cache = driver.run_simulation(ctl, ens, mets, num_devices=4, fused=True,
+                                              timers=Sink(), module_timers=module_timers,
+                                              sort_every=2)
+        assert status == 0
+        outs.append(np.stack([ens.lon, ens.lat, ens.p, ens.time, *ens.q, *cache.uvwp]))
+        if module_timers:
+            timed = list(recs)
+    np.testing.assert_array_equal(outs[0], outs[1])
+    keys = {(gr, n, s) for gr, n, s, _ in timed}
+    for d in range(4):
+        scope = f"device{d}"
+        for mod in driver.PIPELINE + ("generate_random_nums", "module_timesteps"):
+            assert ("PHYSICS", mod, scope) in keys, mod
+        assert ("INIT", "ACC_INIT", scope) in keys
+        assert ("MEMORY", "DELETE_DATA_REGION", scope) in keys
+        fused = sum(ns for gr, n, sc, ns in timed if n == "module_fused_step" and sc == scope)
+        split = sum(ns for gr, n, sc, ns in timed
+                    if gr == "PHYSICS" and n != "module_fused_step" and sc == scope)
+        assert fused > 0 and abs(split - fused) <= 0.01 * fused + 1000
+        adv = sum(ns for gr, n, sc, ns in timed if n == "module_advection" and sc == scope)
+        assert adv > 0
+    assert all(ns >= 0 for *_, ns in timed)
+
+
 def test_met_replication_between_devices(rt):
     """A snapshot one device holds reaches another by GPU-to-GPU copy
     (lt_met_copy_slot), not a second host upload; values identical."""
