@@ -87,6 +87,10 @@ __device__ __forceinline__ void st_state(double* p, double v) { *p = v; }
 #ifndef LT_STEP_MIN_BLOCKS
 #define LT_STEP_MIN_BLOCKS (1024 / LT_STEP_BLOCK)
 #endif
+// resident blocks per SM the exact (FAST = 0) kernels are compiled for
+#ifndef LT_EXACT_MIN_BLOCKS
+#define LT_EXACT_MIN_BLOCKS LT_STEP_MIN_BLOCKS
+#endif
 
 // Arithmetic policy: FAST = 0 reproduces numpy's operation sequence in
 // fp64; FAST = 1 is the mixed-precision path of lt_device.cuh (fp32 store
@@ -320,7 +324,8 @@ __device__ __forceinline__ int64_t row_index(const StepArgs<Rec>& a, int64_t s, 
 // PM: 0 one step, 1 one step applying a pending permutation (PERM), 2
 // a.nsteps steps per particle (MULTI)
 template <class Rec, uint32_t FIXED, int FAST, int RM, int PM>
-__global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel(const StepArgs<Rec> a) {
+__global__ void __launch_bounds__(LT_STEP_BLOCK, FAST ? LT_STEP_MIN_BLOCKS : LT_EXACT_MIN_BLOCKS)
+    step_kernel(const StepArgs<Rec> a) {
   using O = Ops<Rec, FAST>;
   constexpr bool PERM = PM == 1, MULTI = PM == 2;
   const uint32_t mods = FIXED ? FIXED : a.modules;
@@ -475,10 +480,27 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
 
       constexpr uint32_t kNoColumn = 0xFFFFFFFFu;
       uint32_t tcol = kNoColumn;  // lon/lat column of the turb T sample (reused by meso)
-      // exact Philox: the turb and meso normals share block 1 and a pair,
-      // so both streams are drawn at the turb step (meso's kept till then)
-      constexpr bool kBoth = !kEarly && RM == RNG_PHILOX && ((FIXED & (M_TURB | M_MESO)) == (M_TURB | M_MESO));
-      double zmeso[3] = {0.0, 0.0, 0.0};
+      // exact kernels with a compile-time generator: the turb and meso
+      // normals are drawn at ONE call site before the turbulence step (one
+      // inlined copy of the fp64 log / cos / sincospi code instead of two —
+      // the exact kernels stall on instruction fetch); Philox's two streams
+      // also share block 1 and a Box-Muller pair there
+      constexpr bool kBoth = !kEarly && RM >= 0 && ((FIXED & (M_TURB | M_MESO)) == (M_TURB | M_MESO));
+      double zturb[3] = {0.0, 0.0, 0.0}, zmeso[3] = {0.0, 0.0, 0.0};
+      if (kBoth && (want_turb || want_meso) && act) {
+        if (RM == RNG_PHILOX) {
+          philox_turb_meso(ctl.rng_seed_global, stp, gid, zturb, zmeso);
+        } else {
+#pragma unroll 1
+          for (int st = 1; st <= 2; ++st) {
+            double z[3];
+            draws<O, RM>(a, s, gid, st, z, stp);
+            if (st == 1) { zturb[0] = z[0]; zturb[1] = z[1]; zturb[2] = z[2]; }
+            else { zmeso[0] = z[0]; zmeso[1] = z[1]; zmeso[2] = z[2]; }
+          }
+        }
+        LT_CLOCK(CK_RNG);
+      }
 
       // physics.py:119-147 (module_diffusion_turb); the vertical part sees the
       // post-hop lon/lat and pre-hop p (numpy view aliasing)
@@ -488,9 +510,8 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
         if (kEarly) { xt[0] = early[0]; xt[1] = early[1]; xt[2] = early[2]; }
         else
 #endif
-        if (kBoth) philox_turb_meso(ctl.rng_seed_global, stp, gid, xt, zmeso);
-        else draws<O, RM>(a, s, gid, 1, xt, stp);
-        LT_CLOCK(CK_RNG);
+        if (kBoth) { xt[0] = zturb[0]; xt[1] = zturb[1]; xt[2] = zturb[2]; }
+        else { draws<O, RM>(a, s, gid, 1, xt, stp); LT_CLOCK(CK_RNG); }
         if (turb_h) {
           double sig = a.kc.turb_sx;
           if (__builtin_expect(dt != a.kc.dt, 0)) sig = sqrt(2.0 * ctl.turb_dx * dt);
@@ -516,9 +537,8 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, LT_STEP_MIN_BLOCKS) step_kernel
         if (kEarly) { xm[0] = early[3]; xm[1] = early[4]; xm[2] = early[5]; }
         else
 #endif
-        if (kBoth && want_turb) { xm[0] = zmeso[0]; xm[1] = zmeso[1]; xm[2] = zmeso[2]; }
-        else draws<O, RM>(a, s, gid, 2, xm, stp);
-        LT_CLOCK(CK_RNG);
+        if (kBoth) { xm[0] = zmeso[0]; xm[1] = zmeso[1]; xm[2] = zmeso[2]; }
+        else { draws<O, RM>(a, s, gid, 2, xm, stp); LT_CLOCK(CK_RNG); }
         // the vertical hop moved only p: the T sample's lon/lat column holds
         const uint32_t r00 = tcol != kNoColumn ? O::cell_in_column(a.met, tcol, p)
                                                : O::cell(a.met, lon, lat, p);
