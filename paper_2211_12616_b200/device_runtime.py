@@ -96,16 +96,117 @@ class ModelImage:
 
 # ---------------------------------------------------------------- device image
 
+class DeviceRow:
+    """One per-particle field of a device image, indexed like the reference
+    image's numpy array over the GLOBAL particle range (the reference's
+    image is a deep copy of the whole model, device_runtime.py:165-186).
+    The owned range lives in HBM — every access copies that part in or out,
+    in particle order — and the rest is the image's host-side copy, which
+    (as in the reference) is never computed on or copied back.  For tests
+    and inspection; the module API and the driver never go through it."""
+
+    def __init__(self, image: "DeviceImage", fid: int, row: int, shadow: np.ndarray):
+        self.image, self.fid, self.row, self.shadow = image, fid, row, shadow
+
+    def _full(self) -> np.ndarray:
+        img = self.image
+        a = self.shadow.copy()
+        if img.n:
+            a[img.base:img.base + img.n] = img.engine.ctx.d2h_ordered(self.fid, self.row, 0, img.n,
+                                                                      img.base)
+        return a
+
+    def __array__(self, dtype=None, copy=None):
+        a = self._full()
+        return a if dtype is None else a.astype(dtype)
+
+    def __getitem__(self, key):
+        return self._full()[key]
+
+    def __setitem__(self, key, value) -> None:
+        img = self.image
+        a = self._full()
+        a[key] = value
+        self.shadow[:] = a
+        if img.n:
+            img.engine.ctx.h2d_ordered(self.fid, self.row, 0, a[img.base:img.base + img.n], img.base)
+
+    def __len__(self) -> int:
+        return self.shadow.size
+
+    @property
+    def shape(self):
+        return self.shadow.shape
+
+    @property
+    def dtype(self):
+        return self.shadow.dtype
+
+
+class DeviceRows:
+    """A (rows, np) field of a device image (q, uvwp) as a stack of DeviceRow."""
+
+    def __init__(self, rows: list[DeviceRow]):
+        self.rows = rows
+
+    def _full(self) -> np.ndarray:
+        return np.stack([r._full() for r in self.rows])
+
+    def __array__(self, dtype=None, copy=None):
+        a = self._full()
+        return a if dtype is None else a.astype(dtype)
+
+    def __getitem__(self, key):
+        if isinstance(key, (int, np.integer)):
+            return self.rows[key]
+        return self._full()[key]
+
+    def __setitem__(self, key, value) -> None:
+        a = self._full()
+        a[key] = value
+        for r, v in zip(self.rows, a):
+            r[:] = v
+
+    @property
+    def shape(self):
+        return (len(self.rows),) + self.rows[0].shape
+
+
 class DeviceEnsemble:
     """Stand-in for `ParticleEnsemble` inside a device image: the SoA lives
-    in HBM; `np` is the global particle count, as in the reference image."""
+    in HBM; `np` is the global particle count, as in the reference image.
+    time, p, zeta, lon, lat and q read and write like the reference image's
+    arrays (DeviceRow)."""
 
     is_device_resident = True
 
-    def __init__(self, image: "DeviceImage", n_total: int, nq: int):
+    def __init__(self, image: "DeviceImage", n_total: int, nq: int, host_ens=None):
         self.image = image
         self.np = n_total
         self.nq = nq
+        self._rows = {}
+        for name, fid in (("time", capi.F_TIME), ("p", capi.F_P), ("zeta", capi.F_ZETA),
+                          ("lon", capi.F_LON), ("lat", capi.F_LAT)):
+            shadow = np.array(getattr(host_ens, name), dtype=np.float64) if host_ens is not None \
+                else np.zeros(n_total)
+            self._rows[name] = DeviceRow(image, fid, 0, shadow)
+        qh = np.array(host_ens.q, dtype=np.float64) if host_ens is not None else np.zeros((nq, n_total))
+        self._q = DeviceRows([DeviceRow(image, capi.F_Q, k, qh[k].copy()) for k in range(nq)])
+
+    def __getattr__(self, name):
+        rows = self.__dict__.get("_rows", {})
+        if name in rows:
+            return rows[name]
+        if name == "q":
+            return self.__dict__["_q"]
+        raise AttributeError(name)
+
+    def refresh_shadow(self, host_ens) -> None:
+        """The image's copy of particles outside the owned range (upload)."""
+        for name, row in self._rows.items():
+            row.shadow[:] = getattr(host_ens, name)
+        for k, row in enumerate(self._q.rows):
+            row.shadow[:] = host_ens.q[k]
 
 
 class DeviceCache:
@@ -115,8 +216,19 @@ class DeviceCache:
 
     is_device_resident = True
 
-    def __init__(self, image: "DeviceImage"):
+    def __init__(self, image: "DeviceImage", host_cache=None, n_total: int = 0):
         self.image = image
+        uv = np.array(host_cache.uvwp, dtype=np.float64) if host_cache is not None \
+            else np.zeros((3, n_total))
+        iso = np.array(host_cache.iso_var, dtype=np.float64) if host_cache is not None \
+            else np.zeros(n_total)
+        self.uvwp = DeviceRows([DeviceRow(image, capi.F_UVWP, c, uv[c].copy()) for c in range(3)])
+        self.iso_var = DeviceRow(image, capi.F_ISO_VAR, 0, iso)
+
+    def refresh_shadow(self, host_cache) -> None:
+        for c, row in enumerate(self.uvwp.rows):
+            row.shadow[:] = host_cache.uvwp[c]
+        self.iso_var.shadow[:] = host_cache.iso_var
 
     @property
     def iso_nonconverged(self) -> int:
@@ -149,8 +261,8 @@ class DeviceImage:
         self.engine.n = self.n
         self.engine.ctx.ids_reset(0, self.n, self.base)
         self.ctl = deep_copy(host.ctl)
-        self.ens = DeviceEnsemble(self, n_total, nq)
-        self.cache = DeviceCache(self)
+        self.ens = DeviceEnsemble(self, n_total, nq, host.ens)
+        self.cache = DeviceCache(self, host.cache, n_total)
         self.dt = DeviceArray(self, "dt")
         self.batch = DeviceArray(self, "batch")
         self.clim = host.clim
@@ -209,10 +321,12 @@ class DeviceImage:
             for k in range(ens.q.shape[0]):
                 ctx.h2d_ordered(capi.F_Q, k, 0, ens.q[k, s], self.base)
             self.ens.np = int(ens.np)
+            self.ens.refresh_shadow(ens)
         elif name == "cache":
             for c in range(3):
                 ctx.h2d_ordered(capi.F_UVWP, c, 0, host.cache.uvwp[c, s], self.base)
             ctx.h2d_ordered(capi.F_ISO_VAR, 0, 0, host.cache.iso_var[s], self.base)
+            self.cache.refresh_shadow(host.cache)
         elif name == "dt":
             ctx.h2d_ordered(capi.F_DT, 0, 0, np.asarray(host.dt)[s], self.base)
         elif name == "batch":

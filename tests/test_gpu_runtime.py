@@ -206,6 +206,35 @@ def test_fused_mode_timer_contract(rt, golden_chain):
     assert all(ns >= 0 for *_, ns in timed)
 
 
+def test_device_image_fields_read_and_write_like_the_reference_image(rt):
+    """region.image.ens.<field> behaves like the reference image's arrays
+    (device_runtime.py:165-219): the owned range is read from / written to
+    HBM, the rest is the image's own copy, and copy-back moves only the
+    owned range (acceptance c7, test_acceptance.py:205-220)."""
+    dr, _, _, ms, syn = rt
+    from paper_2211_12616_b200.partition import partition_all
+    ens = syn.particles(100, seed=2)
+    host = dr.ModelImage(ctl=ms.Control(), ens=ens, cache=ms.cache_allocate(100),
+                         clim=ms.read_clim(), met0=None, met1=None, dt=np.zeros(100), batch=None)
+    before = ens.lon.copy()
+    with dr.DevicePool(4, debug=True) as pool:
+        ranges = partition_all(100, 4)
+        region = pool.region_create(1, host, ranges[1], with_batch=False)
+        pool.region_update_device(region, host, ("ens", "cache"))
+        np.testing.assert_array_equal(np.asarray(region.image.ens.lon), before)
+        region.image.ens.lon[:] = 999.0
+        assert region.image.ens.lon[30] == 999.0 and region.image.ens.lon[80] == 999.0
+        host.ens.lon[0] += 100.0                      # the image is isolated from the host
+        assert region.image.ens.lon[0] == 999.0
+        region.image.ens.q[2, 26] = 7.0
+        pool.region_update_host(region, host, ranges[1])
+    inside = slice(ranges[1].start, ranges[1].end)
+    assert np.all(host.ens.lon[inside] == 999.0)
+    out = np.r_[1:ranges[1].start, ranges[1].end:100]
+    np.testing.assert_array_equal(host.ens.lon[out], before[out])
+    assert host.ens.q[2, 26] == 7.0 and host.ens.q[2, 80] == 0.0
+
+
 def test_met_replication_between_devices(rt):
     """A snapshot one device holds reaches another by GPU-to-GPU copy
     (lt_met_copy_slot), not a second host upload; values identical."""

@@ -128,3 +128,20 @@ def test_box_keys_order_columns_then_level_pairs():
     brute = np.array([morton(int(a), int(b)) * nb + int(c) // orc.BOX_LEVELS
                       for a, b, c in zip(i, j, k)])
     np.testing.assert_array_equal(keys, brute)
+
+
+def test_clim_hno3_and_tropopause_lookups():
+    """ClimData.hno3 / p_trop (model_state.py:165-180) against the oracle's
+    restatement, including clamped coordinates and grid nodes."""
+    import numpy as np
+    from oracle import lagtrans_oracle as orc
+    from paper_2211_12616_b200.model_state import read_clim
+    clim = read_clim()
+    lg, pg, tab, pt = orc.climatology_tables()
+    rs = np.random.default_rng(4)
+    lat = np.concatenate([rs.uniform(-100, 100, 5000), lg, [-90.0, 90.0]])
+    p = np.concatenate([rs.uniform(0, 1200, 5000), pg[:lg.size], [10.0, 1000.0]])
+    np.testing.assert_allclose(clim.hno3(lat, p), orc.hno3_lookup(lg, pg, tab, lat, p),
+                               rtol=1e-15, atol=0)
+    np.testing.assert_array_equal(clim.p_trop(lat), np.interp(lat, lg, pt))
+    assert clim.hno3(90.0, 50.0) == 0.5e-8
