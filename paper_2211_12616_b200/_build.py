@@ -21,7 +21,7 @@ LIBDIR = PKG / "_lib"
 LIB = LIBDIR / "liblagtrans_b200.so"
 SOURCES = ["lt_capi.cu", "lt_kernels.cu", "lt_step.cu", "lt_output.cu", "lt_host.cpp",
            "lt_comm.cu"]
-HEADERS = ["lt_device.cuh", "lt_step.cuh", "lt_kernels.cuh", "lt_comm.cuh"]
+HEADERS = ["lt_device.cuh", "lt_step.cuh", "lt_kernels.cuh", "lt_comm.cuh", "lt_logtab.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "--expt-relaxed-constexpr",
          "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-v"]

@@ -433,7 +433,11 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, FAST ? LT_STEP_MIN_BLOCKS : LT_
         if (RM == RNG_FAITHFUL) {
           faithful_normals_fast(a.faithful_state, gid - static_cast<uint64_t>(a.faithful_base), early);
         } else if (RM == RNG_PHILOX) {
+#ifdef LT_PROBE_NO_RNG  // timing probe only: what the draws cost
+          for (int q = 0; q < 6; ++q) early[q] = 0.25f * static_cast<float>((gid >> q) & 3) - 0.3f;
+#else
           philox_normals_fast(ctl.rng_seed_global, stp, gid, early);
+#endif
         } else {
           double z[3];
           if (want_turb) {

@@ -443,3 +443,33 @@ def test_close_lon_packing_on_device(b200, path):
     exact(got.interpolate(600.0, lon, lat, p), ref.interpolate(600.0, lon, lat, p))
     ref.close()
     got.close()
+
+
+def test_exact_transcendentals_against_numpy(b200):
+    """The exact kernels' own fp64 log and sin/cos(pi y) (lt_device.cuh
+    lt_log / lt_sincospi2) behind the Box-Muller draws: 1e6 particles of
+    counter-mode draws (6e6 normals through log, sqrt and cos) and 2e5 of
+    faithful draws against the oracle's numpy evaluation, within the
+    contract's 1e-13 relative for values through transcendentals — and
+    1e-14 absolute where cos(2 pi u) crosses zero: numpy rounds the argument
+    2 pi u first, the kernels reduce u exactly (cos_lat's note), so near a
+    zero of the cosine the two differ by ~1e-15 absolute."""
+    _, rng, ms = b200
+    from paper_2211_12616_b200.partition import WorkRange
+    n = 1_000_000
+    st = rng.module_rng_init(ms.Control(rng_mode="counter", rng_seed_global=2211), 1)
+    b = rng.batch_allocate(n)
+    rng.generate_random_nums(st, 17, WorkRange(0, 0, n), 0, b)
+    conv, turb, meso = orc.counter_batch(2211, 17, 0, n)
+    exact(b.convection, conv)
+    np.testing.assert_allclose(b.diff_turb, turb.ravel(), rtol=1e-13, atol=1e-14)
+    np.testing.assert_allclose(b.diff_meso, meso.ravel(), rtol=1e-13, atol=1e-14)
+    m = 200_000
+    stf = rng.module_rng_init(ms.Control(rng_mode="faithful", mpi_rank=5), 1)
+    s0 = stf.device_states[0]
+    bf = rng.batch_allocate(m)
+    rng.generate_random_nums(stf, 0, WorkRange(0, 0, m), 0, bf)
+    fconv, fturb, fmeso, _ = orc.faithful_batch(s0, m)
+    exact(bf.convection, fconv)
+    np.testing.assert_allclose(bf.diff_turb, fturb.ravel(), rtol=1e-13, atol=1e-14)
+    np.testing.assert_allclose(bf.diff_meso, fmeso.ravel(), rtol=1e-13, atol=1e-14)
