@@ -17,15 +17,15 @@ for prec in ("fast", "exact"):
     rep = OUT / f"step_{prec}.ncu-rep"
     summ = subprocess.run([sys.executable, str(ROOT / "tools/ncu_summary.py"), str(rep)],
                           capture_output=True, text=True).stdout
-    (PROF / f"r01_step_{prec}_cfg3.json").write_text(summ)
+    (PROF / f"r02_step_{prec}_cfg3.json").write_text(summ)
     lines = subprocess.run([sys.executable, str(ROOT / "tools/ncu_lines.py"), str(rep), "40"],
                            capture_output=True, text=True).stdout
-    (PROF / f"r01_step_{prec}_cfg3_lines.txt").write_text(lines)
-shutil.copy(OUT / "launches.csv", PROF / "r01_launches_cfg3.csv")
+    (PROF / f"r02_step_{prec}_cfg3_lines.txt").write_text(lines)
+shutil.copy(OUT / "launches.csv", PROF / "r02_launches_cfg3.csv")
 
 out = json.loads((PROF / "ncu_step_cfg3.json").read_text())
 for prec in ("fast", "exact"):
-    d = json.loads((PROF / f"r01_step_{prec}_cfg3.json").read_text())
+    d = json.loads((PROF / f"r02_step_{prec}_cfg3.json").read_text())
     g = lambda k: float(str(d[k]).split()[0])
     dram = (g("dram__bytes_read.sum") + g("dram__bytes_write.sum")) * 1e9
     out[prec].update(duration_ms=g("gpu__time_duration.sum"), dram_bytes_per_launch=dram,
@@ -42,7 +42,7 @@ for prec in ("fast", "exact"):
           list(o["stalls_pct"].items())[:3])
 (PROF / "ncu_step_cfg3.json").write_text(json.dumps(out, indent=1))
 
-rows = list(csv.reader(open(PROF / "r01_launches_cfg3.csv")))
+rows = list(csv.reader(open(PROF / "r02_launches_cfg3.csv")))
 hdr, agg = None, collections.defaultdict(list)
 for r in rows:
     if len(r) > 5 and r[0] == "ID":
