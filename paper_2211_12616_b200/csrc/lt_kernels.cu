@@ -75,15 +75,24 @@ __global__ void rng_fill_kernel(int mode, uint64_t seed_or_state, int64_t step, 
   }
 }
 
-template <class Rec>
+// Box keys from the fast kernels' cell lookup: it returns searchsorted's
+// cells bit for bit (near-node guesses are settled exactly, lt_device.cuh),
+// so the keys — and the stable sort's permutation — are the oracle's
+// box_keys, at a fraction of the fp64 bracketing's cost.  G = 2 on a
+// geographic grid (computed lon/lat cells, log-guessed levels), 1 elsewhere.
+template <class Rec, int G>
 __global__ void box_key_kernel(MetView<Rec> m, const double* lon, const double* lat,
                                const double* p, int64_t start, int64_t n, uint32_t* keys,
                                uint32_t* vals, int morton) {
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t s = start + t;
-    const Cell c = cell_of(m, lon[s], lat[s], p[s]);
-    keys[t] = morton ? box_key_morton(c.i, c.j, c.k, m.nz) : c.r00;
+    float fx, fy, fz;
+    const int i = locate_h<G>(m.lon, __ldcs(lon + s), fx);
+    const int j = locate_h<G>(m.lat, __ldcs(lat + s), fy);
+    const int k = m.nz - 2 - locate_v<G>(m.lev, __ldcs(p + s), fz);
+    const uint32_t r00 = (static_cast<uint32_t>(i) * m.ny + j) * (m.nz - 1) + k;
+    keys[t] = morton ? box_key_morton(i, j, k, m.nz) : r00;
     vals[t] = static_cast<uint32_t>(t);
   }
 }
@@ -244,7 +253,9 @@ template <class Rec>
 cudaError_t launch_box_keys(const MetView<Rec>& m, const double* lon, const double* lat,
                             const double* p, int64_t start, int64_t n, uint32_t* keys,
                             uint32_t* vals, int morton, cudaStream_t st) {
-  box_key_kernel<Rec><<<grid_for(n), 256, 0, st>>>(m, lon, lat, p, start, n, keys, vals, morton);
+  const bool geo = m.lon.uniform && m.lat.uniform && !m.lev.uniform && m.lev.logscale;
+  if (geo) box_key_kernel<Rec, 2><<<grid_for(n), 256, 0, st>>>(m, lon, lat, p, start, n, keys, vals, morton);
+  else box_key_kernel<Rec, 1><<<grid_for(n), 256, 0, st>>>(m, lon, lat, p, start, n, keys, vals, morton);
   return cudaGetLastError();
 }
 template cudaError_t launch_box_keys<RecF>(const MetView<RecF>&, const double*, const double*, const double*, int64_t, int64_t, uint32_t*, uint32_t*, int, cudaStream_t);
