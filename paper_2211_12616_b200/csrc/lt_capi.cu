@@ -51,6 +51,7 @@ struct AxisHost {
   float g0 = 0.f, ginv = 0.f;
   int uniform = 0;
   double dinv = 0.0, dorg = 0.0;
+  std::vector<double2> host_cell;  // host copy of `cell` (the level table in kernel parameters)
 };
 
 struct Slot {
@@ -189,6 +190,7 @@ int upload_axis(AxisHost& ax, const double* x, int n, cudaStream_t st) {
   }
   CK(cudaMemcpyAsync(ax.dev, x, sizeof(double) * n, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(ax.cell, cell.data(), sizeof(double2) * n, cudaMemcpyHostToDevice, st));
+  ax.host_cell = cell;
   CK(cudaStreamSynchronize(st));
   return LT_OK;
 }
@@ -226,6 +228,8 @@ MetView<Rec> met_view(const lt_ctx* c) {
   m.t0 = c->slots[c->use0].t_met;
   m.t1 = c->slots[c->use1].t_met;
   m.inv_dt = m.t1 != m.t0 ? 1.0 / (m.t1 - m.t0) : 0.0;
+  const int ncell = c->ax_lev.n - 1;
+  if (ncell <= kLevCap) std::memcpy(m.levc, c->ax_lev.host_cell.data(), sizeof(double2) * ncell);
   return m;
 }
 

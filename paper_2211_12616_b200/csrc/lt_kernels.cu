@@ -81,7 +81,7 @@ __global__ void rng_fill_kernel(int mode, uint64_t seed_or_state, int64_t step, 
 // box_keys, at a fraction of the fp64 bracketing's cost.  G = 2 on a
 // geographic grid (computed lon/lat cells, log-guessed levels), 1 elsewhere.
 template <class Rec, int G>
-__global__ void box_key_kernel(MetView<Rec> m, const double* lon, const double* lat,
+__global__ void box_key_kernel(const __grid_constant__ MetView<Rec> m, const double* lon, const double* lat,
                                const double* p, int64_t start, int64_t n, uint32_t* keys,
                                uint32_t* vals, int morton) {
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n;
@@ -90,7 +90,7 @@ __global__ void box_key_kernel(MetView<Rec> m, const double* lon, const double* 
     float fx, fy, fz;
     const int i = locate_h<G>(m.lon, __ldcs(lon + s), fx);
     const int j = locate_h<G>(m.lat, __ldcs(lat + s), fy);
-    const int k = m.nz - 2 - locate_v<G>(m.lev, __ldcs(p + s), fz);
+    const int k = m.nz - 2 - locate_v<G>(m.lev, __ldcs(p + s), fz, m.levc);
     const uint32_t r00 = (static_cast<uint32_t>(i) * m.ny + j) * (m.nz - 1) + k;
     keys[t] = morton ? box_key_morton(i, j, k, m.nz) : r00;
     vals[t] = static_cast<uint32_t>(t);
@@ -253,7 +253,8 @@ template <class Rec>
 cudaError_t launch_box_keys(const MetView<Rec>& m, const double* lon, const double* lat,
                             const double* p, int64_t start, int64_t n, uint32_t* keys,
                             uint32_t* vals, int morton, cudaStream_t st) {
-  const bool geo = m.lon.uniform && m.lat.uniform && !m.lev.uniform && m.lev.logscale;
+  const bool geo = m.lon.uniform && m.lat.uniform && !m.lev.uniform && m.lev.logscale &&
+                   m.lev.n - 1 <= kLevCap;
   if (geo) box_key_kernel<Rec, 2><<<grid_for(n), 256, 0, st>>>(m, lon, lat, p, start, n, keys, vals, morton);
   else box_key_kernel<Rec, 1><<<grid_for(n), 256, 0, st>>>(m, lon, lat, p, start, n, keys, vals, morton);
   return cudaGetLastError();
@@ -306,7 +307,8 @@ cudaError_t launch_locate(const MetView<Rec>& m, int fast, const double* lon, co
     locate_kernel<Rec, 0><<<grid_for(n), 256, 0, st>>>(m, lon, lat, p, out, n);
   } else if constexpr (sizeof(Rec) == sizeof(RecF)) {
     // the same dispatch as launch_step: geographic grids get the G = 2 lookups
-    const bool geo = m.lon.uniform && m.lat.uniform && !m.lev.uniform && m.lev.logscale;
+    const bool geo = m.lon.uniform && m.lat.uniform && !m.lev.uniform && m.lev.logscale &&
+                   m.lev.n - 1 <= kLevCap;
     if (geo) locate_kernel<Rec, 2><<<grid_for(n), 256, 0, st>>>(m, lon, lat, p, out, n);
     else locate_kernel<Rec, 1><<<grid_for(n), 256, 0, st>>>(m, lon, lat, p, out, n);
   } else {

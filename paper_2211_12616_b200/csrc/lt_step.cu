@@ -90,7 +90,7 @@ cudaError_t launch_step(const StepArgs<Rec>& a, cudaStream_t st) {
   if constexpr (sizeof(Rec) == sizeof(RecF)) {
     if (a.ctl.precision == 1) {
       const bool geo = a.met.lon.uniform && a.met.lat.uniform && !a.met.lev.uniform &&
-                       a.met.lev.logscale;
+                       a.met.lev.logscale && a.met.lev.n - 1 <= kLevCap;
       return geo ? launch_prec<Rec, 2>(a, st) : launch_prec<Rec, 1>(a, st);
     }
   }

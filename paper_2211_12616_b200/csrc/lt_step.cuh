@@ -219,7 +219,7 @@ struct OpsFast {
 #pragma unroll 1
     for (int it = 0; it < 10 && pending; ++it) {
       float frev;
-      const int krev = locate_v<G>(m.lev, p, frev);
+      const int krev = locate_v<G>(m.lev, p, frev, m.levc);
       const uint32_t r00 = col * dcol + (m.nz - 2 - krev);
       const f32x2 z = pk2(frev, 1.0f - frev);  // (level k, level k+1) weights
       f32x2 a = pk2(0.0f, 0.0f), b = pk2(0.0f, 0.0f);
@@ -256,7 +256,7 @@ struct OpsFast {
   }
   __device__ static uint32_t cell_in_column(const MetView<RecF>& m, uint32_t col, double p) {
     float frev;
-    return col * (m.nz - 1) + (m.nz - 2 - locate_v<G>(m.lev, p, frev));
+    return col * (m.nz - 1) + (m.nz - 2 - locate_v<G>(m.lev, p, frev, m.levc));
   }
   __device__ static void spreads(const MetView<RecF>& m, uint32_t r00, double sig[3]) {
     PairsF q;
@@ -325,7 +325,7 @@ __device__ __forceinline__ int64_t row_index(const StepArgs<Rec>& a, int64_t s, 
 // a.nsteps steps per particle (MULTI)
 template <class Rec, uint32_t FIXED, int FAST, int RM, int PM>
 __global__ void __launch_bounds__(LT_STEP_BLOCK, FAST ? LT_STEP_MIN_BLOCKS : LT_EXACT_MIN_BLOCKS)
-    step_kernel(const StepArgs<Rec> a) {
+    step_kernel(const __grid_constant__ StepArgs<Rec> a) {
   using O = Ops<Rec, FAST>;
   constexpr bool PERM = PM == 1, MULTI = PM == 2;
   const uint32_t mods = FIXED ? FIXED : a.modules;
