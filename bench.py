@@ -7,11 +7,14 @@ Headline workload (BASELINE.json configs[2], the configuration the metric is
 quoted on): **cfg3** — 1e8 particles on the synthetic ERA5-like 0.25 deg grid
 (1440(+1) x 721 x 137), advection + turbulent + mesoscale diffusion
 (+ timesteps, in-kernel Philox draws, position), sharded over N GPUs with the
-reference partition rule, met replicated to every rank by an NCCL
-broadcast.  A "step" is one fused time step of every particle; the box sort
-runs every `--sort-every` steps (15 for cfg3, the measured optimum of
-8/10/15/20; the default 30 timed steps hold exactly two sorts) inside the
-timed region.
+reference partition rule (strong scaling: 1e8 in total; `--scaling weak`
+keeps 1e8 per GPU), met replicated to every GPU by an NCCL broadcast.  N > 1
+runs either as torchrun ranks (one GPU each) or, without torchrun, as ONE
+process driving N GPUs (the paper's design; lt_met_broadcast).  A "step" is
+one fused time step of every particle; the box sort runs every
+`--sort-every` steps (15 for cfg3, the measured optimum — flat from 15 to
+25; the default 30 timed steps hold exactly two sorts) inside the timed
+region.
 
 Other workloads (parity shapes, informational lines): cfg1 (SBR, 1e5,
 advection), cfg2 (1e7, 1 deg), cfg4 (5e7 volcanic point release, advection
@@ -20,9 +23,11 @@ host memory every simulated hour = every 20 steps, inside the timed region),
 cfg5 (5e8 particles, the full module chain + decay, sort every 10 steps).
 
 `value` is device-timed (CUDA events on the engine stream, max over ranks,
-inputs resident in HBM).  `e2e` is the public host-buffer API
+inputs resident in HBM); `roofline.achieved` counts SURVEY.md 8(d)'s
+algorithmic bytes per particle-step.  `e2e` is the public host-buffer API
 (Engine.step_host -> lt_run_host): the shard's SoA in pinned host memory
-streams in, steps and streams out every step.  `cpu_baseline` and `--impl
+streams in, steps and streams out every step; the line carries the host
+link's measured ceiling beside it.  `cpu_baseline` and `--impl
 reference` time the CPU oracle (a numpy restatement of the reference,
 oracle/) on the host's cores on a bounded particle sample of the same
 workload.  `precision` "fast" (default) computes interpolation weights and
@@ -34,9 +39,12 @@ packs only 24 bits of index, so at 1e8 particles it would hand particles i
 and i + 2^24 identical draws; `counter` reproduces the reference's words
 bit for bit.  The line also carries the same measurement with the
 bit-faithful "exact" kernels (`alt_precision`), with the counter words
-(`alt_rng`), and with the steps between two sorts run as one multi-step
-launch each (`alt_multistep`, Engine.step_many; identical results).  The
-headline is one launch per step, the unit its roofline is stated for.
+(`alt_rng`), with both — the like-for-like, fully reference-faithful
+configuration (`alt_reference_faithful`) — and with the steps between two
+sorts run as one multi-step launch each (`alt_multistep`, Engine.step_many;
+identical results).  The headline is one launch per step, the unit its
+roofline is stated for.  The reference arm builds its inputs without
+importing the product package and reports `product_code_loaded`.
 """
 
 from __future__ import annotations
