@@ -125,32 +125,56 @@ def golden_sbr():
     return load_golden("sbr")
 
 
-def hires_met_pair(g):
-    """The 0.25 deg x 137-level window of hires.npz: met rebuilt from the
-    stored axes by tests/golden/hires_met.py (the fields are too large to
-    commit), checked byte for byte against the digest of the fields the
-    reference ran on."""
+def hires_met_pair(g, phases=(0.0, 5.0), lon_scale=20.0, periodic=False):
+    """The met of hires.npz (0.25 deg x 137-level window) or deg1.npz (global
+    1 deg x 60, closed by met_periodic): rebuilt from the stored axes by
+    tests/golden/hires_met.py (the fields are too large to commit), checked
+    byte for byte against the digest of the fields the reference ran on."""
     sys.path.insert(0, str(GOLDEN))
     import hires_met as hm
     lons, lats, levs = g["lons"], g["lats"], g["levs"]
     snaps = []
-    for t, phase, dig in ((0.0, 0.0, "digest0"), (10800.0, 5.0, "digest1")):
-        f = hm.fields(lons, lats, levs, phase)
-        assert hm.fields_digest(f) == str(g[dig]), "hires met rebuilt differently"
-        snaps.append(orc.Snapshot(t, lons, lats, levs, f["u"], f["v"], f["w"], f["T"]))
+    for t, phase, dig in ((0.0, phases[0], "digest0"), (10800.0, phases[1], "digest1")):
+        f = hm.fields(lons, lats, levs, phase, lon_scale=lon_scale)
+        assert hm.fields_digest(f) == str(g[dig]), "golden met rebuilt differently"
+        snap = orc.Snapshot(t, lons, lats, levs, f["u"], f["v"], f["w"], f["T"])
+        snaps.append(orc.close_longitudes(snap) if periodic else snap)
     return snaps
+
+
+STAGES = ("in", "timesteps", "isoinit", "advection", "turb", "meso", "convection", "sedi",
+          "preiso", "isosurf", "preposition", "position", "meteo", "isopressure")
+
+
+def restore_stages(g):
+    """Undo make_golden.dedupe_stages: a stage's missing array is the
+    previous stage's."""
+    out = dict(g)
+    for f in ("time", "p", "zeta", "lon", "lat", "q", "uvwp", "iso", "dt"):
+        prev = None
+        for tag in STAGES:
+            k = f"{tag}_{f}"
+            if k in out:
+                prev = out[k]
+            elif prev is not None:
+                out[k] = prev
+    return out
 
 
 def golden_module_set(name):
     """(golden dict, Control, met0, met1) of a module-pairs fixture:
-    "modules" (10 x 5 deg x 20, modules.npz) or "hires" (the headline
-    0.25 deg x 137-level shape, hires.npz; keys under "mod_")."""
+    "modules" (10 x 5 deg x 20, modules.npz), "hires" (the headline
+    0.25 deg x 137-level shape, hires.npz) or "deg1" (cfg1/cfg2's global
+    1 deg x 60 grid, deg1.npz); keys under "mod_" in the last two."""
     if name == "modules":
         g = load_golden("modules")
         return g, modules_ctl(), snapshot_from(g, "m0"), snapshot_from(g, "m1")
-    h = load_golden("hires")
-    g = {k[4:]: v for k, v in h.items() if k.startswith("mod_")}
-    m0, m1 = hires_met_pair(h)
+    h = load_golden(name)
+    g = restore_stages({k[4:]: v for k, v in h.items() if k.startswith("mod_")})
+    if name == "hires":
+        m0, m1 = hires_met_pair(h)
+    else:   # deg1
+        m0, m1 = hires_met_pair(h, phases=(0.0, 7.0), lon_scale=180.0, periodic=True)
     return g, modules_ctl(), m0, m1
 
 

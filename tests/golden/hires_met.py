@@ -1,4 +1,6 @@
-"""Met recipe of the 0.25 deg x 137-level golden fixture (hires.npz).
+"""Met recipe of the 0.25 deg x 137-level golden fixture (hires.npz) and of
+the global 1 deg x 60-level one (deg1.npz, with lon_scale = 180 and the
++360 column of met_periodic appended as a copy of column 0).
 
 The fixture is the headline grid's shape — 0.25 deg spacing and all 137
 levels of geomspace(1013.25, 0.01, 137) — on a 40 x 40 deg window
@@ -39,9 +41,10 @@ def axes():
     return lons, lats, levs
 
 
-def fields(lons, lats, levs, phase=0.0):
-    """u, v, w, T as float32-valued float64 (nx, ny, nz) arrays."""
-    X = ((np.asarray(lons, dtype=np.float64) + phase) / 20.0)[:, None, None]
+def fields(lons, lats, levs, phase=0.0, lon_scale=20.0):
+    """u, v, w, T as float32-valued float64 (nx, ny, nz) arrays.  lon_scale
+    180 keeps the longitude polynomial O(1) on a global grid (deg1.npz)."""
+    X = ((np.asarray(lons, dtype=np.float64) + phase) / lon_scale)[:, None, None]
     Y = (np.asarray(lats, dtype=np.float64) / 90.0)[None, :, None]
     Z = (np.asarray(levs, dtype=np.float64) / 1000.0)[None, None, :]
     c = 1.0 - Y * Y                           # cos-like in latitude

@@ -179,6 +179,30 @@ def module_pairs(ctl, m0, m1, ens, seed=12, lon_span=(-900.0, 900.0)):
     return rec
 
 
+STAGES = ("in", "timesteps", "isoinit", "advection", "turb", "meso", "convection", "sedi",
+          "preiso", "isosurf", "preposition", "position", "meteo", "isopressure")
+FIELDS = ("time", "p", "zeta", "lon", "lat", "q", "uvwp", "iso", "dt")
+
+
+def dedupe_stages(rec, prefix=""):
+    """Drop a stage's array when it equals the previous stage's (most modules
+    change one or two fields); tests/conftest.py:golden_module_set restores
+    them.  Keeps the fixtures small."""
+    out = dict(rec)
+    for f in FIELDS:
+        prev = None
+        for tag in STAGES:
+            k = f"{prefix}{tag}_{f}"
+            if k not in out:
+                continue
+            if prev is not None and np.array_equal(out[k], prev, equal_nan=True):
+                cur = out.pop(k)
+            else:
+                cur = out[k]
+            prev = cur
+    return out
+
+
 def gen_hires():
     """The headline grid's shape (0.25 deg, all 137 levels down to 0.01 hPa)
     on a 40 x 40 deg window (hires_met.py): every module once from
@@ -219,8 +243,34 @@ def gen_hires():
     np.savez_compressed(OUT / "hires.npz", lons=lons, lats=lats, levs=levs,
                         digest0=np.array(hm.fields_digest(f0)),
                         digest1=np.array(hm.fields_digest(f1)),
-                        **rec, **init, **ens_arrays("chain_final", ens),
+                        **dedupe_stages(rec, "mod_"), **init, **ens_arrays("chain_final", ens),
                         chain_final_uvwp=cache.uvwp)
+
+
+def gen_deg1():
+    """cfg1/cfg2's grid in full — 1 deg x 60 levels (geomspace(1013.25, 1,
+    60)), global, closed by met_periodic — every module once from identical
+    inputs (module_pairs), 1e4 particles."""
+    sys.path.insert(0, str(OUT))
+    import hires_met as hm
+    lons = f32(np.arange(-180.0, 180.0, 1.0))
+    lats = f32(np.linspace(-90.0, 90.0, 181))
+    levs = f32(np.geomspace(1013.25, 1.0, 60))
+    f0 = hm.fields(lons, lats, levs, 0.0, lon_scale=180.0)
+    f1 = hm.fields(lons, lats, levs, 7.0, lon_scale=180.0)
+    m0 = ingest.met_periodic(MeteoField(t_met=0.0, lons=lons, lats=lats, levs=levs, **f0))
+    m1 = ingest.met_periodic(MeteoField(t_met=10800.0, lons=lons, lats=lats, levs=levs, **f1))
+    ctl = modules_control()
+    ens = particles(ctl, 10000, 41, lat_span=90.0)
+    rs = np.random.default_rng(42)
+    ens.lon[:500] = f32(rs.choice(lons, 500))            # on nodes, incl. the seam
+    ens.lon[500:520] = [180.0, -180.0, 179.5, 179.99998, -179.99998] * 4
+    ens.p[:1000] = f32(np.exp(rs.uniform(np.log(0.5), np.log(1100.0), 1000)))
+    rec = module_pairs(ctl, m0, m1, ens, seed=43)
+    rec = {f"mod_{k}": v for k, v in rec.items() if not k.startswith(("m0_", "m1_"))}
+    np.savez_compressed(OUT / "deg1.npz", lons=lons, lats=lats, levs=levs,
+                        digest0=np.array(hm.fields_digest(f0)),
+                        digest1=np.array(hm.fields_digest(f1)), **dedupe_stages(rec, "mod_"))
 
 
 def gen_rng():
@@ -364,7 +414,7 @@ def gen_output():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["interp", "modules", "rng", "chain", "sbr", "output", "hires"]
+    which = sys.argv[1:] or ["interp", "modules", "rng", "chain", "sbr", "output", "hires", "deg1"]
     for name in which:
         globals()[f"gen_{name}"]()
         print("wrote", name)

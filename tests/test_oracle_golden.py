@@ -109,7 +109,7 @@ def _state(g, tag):
             if f"{tag}_{k}" in g}
 
 
-@pytest.fixture(scope="module", params=["modules", "hires"])
+@pytest.fixture(scope="module", params=["modules", "hires", "deg1"])
 def mods(request):
     """Every stage on the 10 x 5 deg x 20 fixture and on the headline
     0.25 deg x 137-level window (levels down to 0.01 hPa)."""
