@@ -101,19 +101,35 @@ class DeviceRow:
     image's numpy array over the GLOBAL particle range (the reference's
     image is a deep copy of the whole model, device_runtime.py:165-186).
     The owned range lives in HBM — every access copies that part in or out,
-    in particle order — and the rest is the image's host-side copy, which
-    (as in the reference) is never computed on or copied back.  For tests
-    and inspection; the module API and the driver never go through it."""
+    in particle order — and the particles outside it are the image's
+    host-side copy (`outside`: the rows before and after the owned range
+    only, so a one-device image holds none), which, as in the reference, is
+    never computed on or copied back.  For tests and inspection; the module
+    API and the driver never go through it."""
 
-    def __init__(self, image: "DeviceImage", fid: int, row: int, shadow: np.ndarray):
-        self.image, self.fid, self.row, self.shadow = image, fid, row, shadow
+    def __init__(self, image: "DeviceImage", fid: int, row: int, host_row=None,
+                 n_total: int = 0):
+        self.image, self.fid, self.row = image, fid, row
+        self.n_total = int(n_total if host_row is None else np.asarray(host_row).size)
+        self.before = np.zeros(image.base)
+        self.after = np.zeros(max(self.n_total - image.base - image.n, 0))
+        if host_row is not None:
+            self.refresh(host_row)
+
+    def refresh(self, host_row) -> None:
+        img = self.image
+        h = np.asarray(host_row, dtype=np.float64)
+        self.before[:] = h[:img.base]
+        self.after[:] = h[img.base + img.n:]
 
     def _full(self) -> np.ndarray:
         img = self.image
-        a = self.shadow.copy()
+        a = np.empty(self.n_total)
+        a[:img.base] = self.before
+        a[img.base + img.n:] = self.after
         if img.n:
-            a[img.base:img.base + img.n] = img.engine.ctx.d2h_ordered(self.fid, self.row, 0, img.n,
-                                                                      img.base)
+            img.engine.ctx.d2h_ordered(self.fid, self.row, 0, img.n, img.base,
+                                       out=a[img.base:img.base + img.n])
         return a
 
     def __array__(self, dtype=None, copy=None):
@@ -127,20 +143,20 @@ class DeviceRow:
         img = self.image
         a = self._full()
         a[key] = value
-        self.shadow[:] = a
+        self.refresh(a)
         if img.n:
             img.engine.ctx.h2d_ordered(self.fid, self.row, 0, a[img.base:img.base + img.n], img.base)
 
     def __len__(self) -> int:
-        return self.shadow.size
+        return self.n_total
 
     @property
     def shape(self):
-        return self.shadow.shape
+        return (self.n_total,)
 
     @property
     def dtype(self):
-        return self.shadow.dtype
+        return np.dtype(np.float64)
 
 
 class DeviceRows:
@@ -187,11 +203,11 @@ class DeviceEnsemble:
         self._rows = {}
         for name, fid in (("time", capi.F_TIME), ("p", capi.F_P), ("zeta", capi.F_ZETA),
                           ("lon", capi.F_LON), ("lat", capi.F_LAT)):
-            shadow = np.array(getattr(host_ens, name), dtype=np.float64) if host_ens is not None \
-                else np.zeros(n_total)
-            self._rows[name] = DeviceRow(image, fid, 0, shadow)
-        qh = np.array(host_ens.q, dtype=np.float64) if host_ens is not None else np.zeros((nq, n_total))
-        self._q = DeviceRows([DeviceRow(image, capi.F_Q, k, qh[k].copy()) for k in range(nq)])
+            h = getattr(host_ens, name) if host_ens is not None else None
+            self._rows[name] = DeviceRow(image, fid, 0, h, n_total)
+        self._q = DeviceRows([DeviceRow(image, capi.F_Q, k,
+                                        host_ens.q[k] if host_ens is not None else None, n_total)
+                              for k in range(nq)])
 
     def __getattr__(self, name):
         rows = self.__dict__.get("_rows", {})
@@ -204,9 +220,9 @@ class DeviceEnsemble:
     def refresh_shadow(self, host_ens) -> None:
         """The image's copy of particles outside the owned range (upload)."""
         for name, row in self._rows.items():
-            row.shadow[:] = getattr(host_ens, name)
+            row.refresh(getattr(host_ens, name))
         for k, row in enumerate(self._q.rows):
-            row.shadow[:] = host_ens.q[k]
+            row.refresh(host_ens.q[k])
 
 
 class DeviceCache:
@@ -218,17 +234,17 @@ class DeviceCache:
 
     def __init__(self, image: "DeviceImage", host_cache=None, n_total: int = 0):
         self.image = image
-        uv = np.array(host_cache.uvwp, dtype=np.float64) if host_cache is not None \
-            else np.zeros((3, n_total))
-        iso = np.array(host_cache.iso_var, dtype=np.float64) if host_cache is not None \
-            else np.zeros(n_total)
-        self.uvwp = DeviceRows([DeviceRow(image, capi.F_UVWP, c, uv[c].copy()) for c in range(3)])
-        self.iso_var = DeviceRow(image, capi.F_ISO_VAR, 0, iso)
+        hc = host_cache
+        self.uvwp = DeviceRows([DeviceRow(image, capi.F_UVWP, c,
+                                          hc.uvwp[c] if hc is not None else None, n_total)
+                                for c in range(3)])
+        self.iso_var = DeviceRow(image, capi.F_ISO_VAR, 0, hc.iso_var if hc is not None else None,
+                                 n_total)
 
     def refresh_shadow(self, host_cache) -> None:
         for c, row in enumerate(self.uvwp.rows):
-            row.shadow[:] = host_cache.uvwp[c]
-        self.iso_var.shadow[:] = host_cache.iso_var
+            row.refresh(host_cache.uvwp[c])
+        self.iso_var.refresh(host_cache.iso_var)
 
     @property
     def iso_nonconverged(self) -> int:
@@ -355,15 +371,23 @@ class DeviceImage:
         n = hi - lo
         if lo != 0 or hi != self.n:
             raise LifecycleError("copy-back must cover the device's whole range")
-        get = lambda fid, row=0: ctx.d2h_ordered(fid, row, 0, n, self.base)
+        def get(dst, fid, row=0):
+            # straight into the caller's row when it is a contiguous float64
+            # slice (pinned host memory then moves at full PCIe rate)
+            v = dst[s]
+            if v.flags.c_contiguous and v.dtype == np.float64:
+                ctx.d2h_ordered(fid, row, 0, n, self.base, out=v)
+            else:
+                dst[s] = ctx.d2h_ordered(fid, row, 0, n, self.base)
         ens = host.ens
-        ens.time[s], ens.p[s], ens.zeta[s] = get(capi.F_TIME), get(capi.F_P), get(capi.F_ZETA)
-        ens.lon[s], ens.lat[s] = get(capi.F_LON), get(capi.F_LAT)
+        for name, fid in (("time", capi.F_TIME), ("p", capi.F_P), ("zeta", capi.F_ZETA),
+                          ("lon", capi.F_LON), ("lat", capi.F_LAT)):
+            get(getattr(ens, name), fid)
         for k in range(min(ens.q.shape[0], ctx.nq)):
-            ens.q[k, s] = get(capi.F_Q, k)
+            get(ens.q[k], capi.F_Q, k)
         for c in range(3):
-            host.cache.uvwp[c, s] = get(capi.F_UVWP, c)
-        host.cache.iso_var[s] = get(capi.F_ISO_VAR)
+            get(host.cache.uvwp[c], capi.F_UVWP, c)
+        get(host.cache.iso_var, capi.F_ISO_VAR)
 
     def close(self) -> None:
         self.engine.close()

@@ -77,7 +77,7 @@ DEFAULT_SORT_EVERY = 15   # measured optimum at cfg3
 def run_simulation(ctl, ens, mets, num_devices: int = 1, *, fused: bool = True,
                    modules: int | None = None, sort_every: int | None = None, clim=None,
                    timers=None, on_output=None, parallel: bool = True,
-                   device_map=None, module_timers: bool = False):
+                   device_map=None, module_timers: bool = False, cache=None):
     """Advance `ens` (host ParticleEnsemble, updated in place at every
     output time) from ctl.t_start to ctl.t_stop.  Returns (status, cache):
     status 0 on success, 1 when a device task failed (driver_cli.py:196-199).
@@ -101,7 +101,8 @@ def run_simulation(ctl, ens, mets, num_devices: int = 1, *, fused: bool = True,
     if modules is None:
         modules = eng.FULL
     met0, met1, rest = bracketing(list(mets), ctl.t_start)
-    cache = cache_allocate(ens.np)
+    if cache is None:   # (a caller may pass its own, e.g. in pinned host memory)
+        cache = cache_allocate(ens.np)
     host = ModelImage(ctl=ctl, ens=ens, cache=cache, clim=clim, met0=met0, met1=met1,
                       dt=np.zeros(ens.np), batch=batch_allocate(ens.np) if not fused else None)
     rng = module_rng_init(ctl, num_devices)
