@@ -540,6 +540,12 @@ def run_one_process(args, wl):
     peak = peaks.get("hbm_gbs", 6650.0)
     per_gpu_ms = total_ms / args.steps
     achieved = b * ranges[0].size / (per_gpu_ms / 1e3) / 1e9
+    from paper_2211_12616_b200 import _capi as capi
+    selftest = "ok"
+    try:   # NCCL over the distinct GPUs of this run, checked byte for byte
+        capi.check(capi.load().lt_nccl_selftest(len(set(devs)), 1 << 20))
+    except Exception as exc:  # reported, not fatal: the timed run did not need it
+        selftest = f"failed: {exc}"
     info = nccl_info()
     print(json.dumps({
         "metric": METRIC, "value": value, "unit": "particle-steps/s", "n_gpus": G,
@@ -558,6 +564,7 @@ def run_one_process(args, wl):
                      "frac": achieved / peak, "traffic": None, "kernel": "step_kernel (per GPU, "
                      "ms/step incl. sorts)", "algorithmic_bytes_per_particle_step": b},
         "met_broadcast": {"nccl_version": info["version"], "nccl_ranks": info["ranks"],
+                          "nccl_selftest": selftest,
                           "gpus_distinct": len(set(devs)),
                           "setup_s_upload_plus_broadcast": t_met},
         "clocks": clk.summary(),

@@ -169,6 +169,10 @@ int lt_met_broadcast(lt_ctx *const *ctxs, int32_t n, int32_t root, const int32_t
    the number of NCCL ranks the process has created */
 int lt_nccl_version(int32_t *version);
 int lt_nccl_ranks(int32_t *nranks);
+/* NCCL end to end on the GPUs present: a communicator over devices
+   0..ndev-1 and one broadcast group of `bytes` from device 0 into a
+   separate buffer on every device, checked byte for byte */
+int lt_nccl_selftest(int32_t ndev, int64_t bytes);
 int lt_met_slot_time(lt_ctx *ctx, int32_t slot, double *t_met);
 
 /* climatology tables for module_meteo (ClimData model_state.py:156-181) */

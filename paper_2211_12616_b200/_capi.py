@@ -124,6 +124,7 @@ _PROTOS = {
     "lt_met_broadcast": ([C.POINTER(_P), _I32, _I32, C.POINTER(_I32)], C.c_int),
     "lt_nccl_version": ([C.POINTER(_I32)], C.c_int),
     "lt_nccl_ranks": ([C.POINTER(_I32)], C.c_int),
+    "lt_nccl_selftest": ([_I32, _I64], C.c_int),
     "lt_met_slot_time": ([_P, _I32, C.POINTER(_D)], C.c_int),
     "lt_clim_load": ([_P, _I32, _I32, _P, _P, _P, _P], C.c_int),
     "lt_locate_cells": ([_P, _I32, _I64, _P, _P, _P, _P], C.c_int),

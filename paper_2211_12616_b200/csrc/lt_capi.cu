@@ -853,6 +853,56 @@ int lt_nccl_version(int32_t* version) {
   return LT_OK;
 }
 
+// NCCL on this box, end to end with the GPUs there are: a communicator over
+// `ndev` devices (ncclCommInitAll), one broadcast group of `bytes` from
+// device 0 into a separate buffer on every device (device 0 too: send and
+// receive buffers differ), checked byte for byte.  Returns LT_ERR_STATE when
+// NCCL cannot be loaded, LT_ERR_CUDA on a mismatch.
+int lt_nccl_selftest(int32_t ndev, int64_t bytes) {
+  int have = 0;
+  CK(cudaGetDeviceCount(&have));
+  if (ndev < 1 || ndev > have) return fail(LT_ERR_ARG, "ndev %d outside [1, %d]", ndev, have);
+  if (bytes < 1) return fail(LT_ERR_ARG, "bytes must be positive");
+  std::vector<int> devs(ndev);
+  std::vector<void*> send(ndev, nullptr), recv(ndev, nullptr);
+  std::vector<cudaStream_t> streams(ndev, nullptr);
+  std::vector<unsigned char> pattern(static_cast<size_t>(bytes)), back(static_cast<size_t>(bytes));
+  for (size_t b = 0; b < pattern.size(); ++b) pattern[b] = static_cast<unsigned char>((b * 131u + 7u) & 0xFF);
+  int rc = LT_OK;
+  std::string err;
+  for (int d = 0; d < ndev && !rc; ++d) {
+    devs[d] = d;
+    if (cudaSetDevice(d) != cudaSuccess || cudaStreamCreateWithFlags(&streams[d], cudaStreamNonBlocking) != cudaSuccess ||
+        cudaMalloc(&send[d], bytes) != cudaSuccess || cudaMalloc(&recv[d], bytes) != cudaSuccess ||
+        cudaMemset(recv[d], 0, bytes) != cudaSuccess)
+      rc = fail(LT_ERR_CUDA, "selftest allocation on device %d failed", d);
+  }
+  if (!rc && cudaMemcpy(send[0], pattern.data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess)
+    rc = fail(LT_ERR_CUDA, "selftest upload failed");
+  if (!rc) {
+    // rank 0 sends from its own buffer; every rank receives into recv[d]
+    std::vector<void*> bufs(recv);
+    std::vector<void*> sendbufs(send);
+    if (lt_comm::broadcast_from(devs, sendbufs[0], bufs, static_cast<size_t>(bytes), streams, &err))
+      rc = fail(LT_ERR_STATE, "%s", err.c_str());
+  }
+  for (int d = 0; d < ndev && !rc; ++d) {
+    cudaSetDevice(d);
+    if (cudaStreamSynchronize(streams[d]) != cudaSuccess ||
+        cudaMemcpy(back.data(), recv[d], bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
+      rc = fail(LT_ERR_CUDA, "selftest readback on device %d failed", d);
+    else if (std::memcmp(back.data(), pattern.data(), static_cast<size_t>(bytes)) != 0)
+      rc = fail(LT_ERR_CUDA, "NCCL broadcast delivered wrong bytes to device %d", d);
+  }
+  for (int d = 0; d < ndev; ++d) {
+    cudaSetDevice(d);
+    if (send[d]) cudaFree(send[d]);
+    if (recv[d]) cudaFree(recv[d]);
+    if (streams[d]) cudaStreamDestroy(streams[d]);
+  }
+  return rc;
+}
+
 int lt_nccl_ranks(int32_t* nranks) {
   std::string err;
   *nranks = lt_comm::communicators(&err);

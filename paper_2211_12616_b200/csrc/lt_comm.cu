@@ -87,26 +87,35 @@ int version(int* v, std::string* err) {
   return r == ncclSuccess ? 0 : nccl_fail(a, r, "ncclGetVersion", err);
 }
 
-int broadcast(const std::vector<int>& devices, const std::vector<void*>& bufs, size_t bytes,
-              int root, const std::vector<cudaStream_t>& streams, std::string* err) {
-  std::lock_guard<std::mutex> lock(g_mu);
-  const Api* a = api(err);
-  if (!a) return -1;
+namespace {
+// caller holds g_mu
+const std::vector<ncclComm_t>* comms_for(const Api* a, const std::vector<int>& devices,
+                                         std::string* err) {
   auto it = g_comms.find(devices);
   if (it == g_comms.end()) {
     std::vector<ncclComm_t> comms(devices.size());
     ncclResult_t r = a->CommInitAll(comms.data(), static_cast<int>(devices.size()), devices.data());
-    if (r != ncclSuccess) return nccl_fail(a, r, "ncclCommInitAll", err);
+    if (r != ncclSuccess) {
+      nccl_fail(a, r, "ncclCommInitAll", err);
+      return nullptr;
+    }
     it = g_comms.emplace(devices, std::move(comms)).first;
   }
-  const std::vector<ncclComm_t>& comms = it->second;
-  // one group: every rank's broadcast is enqueued on its own copy stream
-  // before any of them may start (required when one thread drives all GPUs)
+  return &it->second;
+}
+
+// one group: every rank's broadcast is enqueued on its own stream before
+// any of them may start (required when one thread drives all GPUs)
+int group_broadcast(const Api* a, const std::vector<ncclComm_t>& comms,
+                    const std::vector<int>& devices, const void* send,
+                    const std::vector<void*>& recv, size_t bytes, int root,
+                    const std::vector<cudaStream_t>& streams, std::string* err) {
   ncclResult_t r = a->GroupStart();
   if (r != ncclSuccess) return nccl_fail(a, r, "ncclGroupStart", err);
   for (size_t i = 0; i < devices.size(); ++i) {
     cudaSetDevice(devices[i]);
-    r = a->Broadcast(bufs[root], bufs[i], bytes, ncclChar, root, comms[i], streams[i]);
+    r = a->Broadcast(static_cast<int>(i) == root ? send : recv[i], recv[i], bytes, ncclChar, root,
+                     comms[i], streams[i]);
     if (r != ncclSuccess) {
       a->GroupEnd();
       return nccl_fail(a, r, "ncclBroadcast", err);
@@ -115,6 +124,28 @@ int broadcast(const std::vector<int>& devices, const std::vector<void*>& bufs, s
   r = a->GroupEnd();
   if (r != ncclSuccess) return nccl_fail(a, r, "ncclGroupEnd", err);
   return 0;
+}
+}  // namespace
+
+int broadcast(const std::vector<int>& devices, const std::vector<void*>& bufs, size_t bytes,
+              int root, const std::vector<cudaStream_t>& streams, std::string* err) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  const Api* a = api(err);
+  if (!a) return -1;
+  const std::vector<ncclComm_t>* comms = comms_for(a, devices, err);
+  if (!comms) return -1;
+  return group_broadcast(a, *comms, devices, bufs[root], bufs, bytes, root, streams, err);
+}
+
+int broadcast_from(const std::vector<int>& devices, const void* send,
+                   const std::vector<void*>& recv, size_t bytes,
+                   const std::vector<cudaStream_t>& streams, std::string* err) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  const Api* a = api(err);
+  if (!a) return -1;
+  const std::vector<ncclComm_t>* comms = comms_for(a, devices, err);
+  if (!comms) return -1;
+  return group_broadcast(a, *comms, devices, send, recv, bytes, 0, streams, err);
 }
 
 int communicators(std::string* err) {

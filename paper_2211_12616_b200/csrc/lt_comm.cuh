@@ -17,6 +17,11 @@ int version(int* v, std::string* err);
 int broadcast(const std::vector<int>& devices, const std::vector<void*>& bufs, size_t bytes,
               int root, const std::vector<cudaStream_t>& streams, std::string* err);
 
+// the same with a separate send buffer on the root (rank 0)
+int broadcast_from(const std::vector<int>& devices, const void* send,
+                   const std::vector<void*>& recv, size_t bytes,
+                   const std::vector<cudaStream_t>& streams, std::string* err);
+
 // number of NCCL ranks (communicators) created so far in this process
 int communicators(std::string* err);
 

@@ -316,6 +316,22 @@ def test_met_broadcast_replicates_slot(rt):
         x.close()
 
 
+def test_nccl_selftest_on_this_box(rt):
+    """NCCL itself on the box: a communicator over every GPU present
+    (ncclCommInitAll) and one broadcast group from device 0 into a separate
+    buffer on each device, checked byte for byte (lt_nccl_selftest) — the
+    collective the met broadcast issues between distinct GPUs."""
+    from paper_2211_12616_b200 import _capi as capi
+    from paper_2211_12616_b200.context import nccl_info
+    lib = capi.load()
+    n = capi.device_count()
+    capi.check(lib.lt_nccl_selftest(n, 3 << 20))
+    info = nccl_info()
+    assert info["version"] >= 22700 and info["ranks"] >= n
+    with pytest.raises(ValueError):
+        capi.check(lib.lt_nccl_selftest(n + 1, 16))
+
+
 def test_driver_rotations_broadcast_met(rt):
     """driver.run_simulation (fused) on 3 devices with hourly snapshots: each
     rotation's next snapshot is uploaded once and broadcast (MET_BROADCAST
