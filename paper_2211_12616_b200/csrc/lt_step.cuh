@@ -210,33 +210,38 @@ struct OpsFast {
     const uint32_t col = static_cast<uint32_t>(i) * m.ny + j;
     const float gx = 1.0f - fx, gy = 1.0f - fy;
     const float xy[4] = {gx * gy, fx * gy, gx * fy, fx * fy};
-    const bool two = m.t1 != m.t0;
-    float wt = two ? static_cast<float>((time - m.t0) * m.inv_dt) : 0.0f;
+    const float wt = static_cast<float>((time - m.t0) * m.inv_dt);
     const f32x2 w2 = bc2(fminf(fmaxf(wt, 0.0f), 1.0f));
     const float inv_theta0 = rcp_approx(static_cast<float>(theta0));
     const uint32_t dcol = m.nz - 1, drow = static_cast<uint32_t>(m.ny) * dcol;
     bool pending = true;
+    // the column's T at the two levels of the current level cell, already
+    // weighted over the 4 columns and blended in time: the iteration moves
+    // only p, so while p stays in that cell (most iterations) T(p) is one
+    // FMA on (T(k), T(k+1)) and the records are not gathered again
+    int kcell = -1;
+    f32x2 tz = pk2(0.0f, 0.0f);
 #pragma unroll 1
     for (int it = 0; it < 10 && pending; ++it) {
       float frev;
       const int krev = locate_v<G>(m.lev, p, frev, m.levc);
-      const uint32_t r00 = col * dcol + (m.nz - 2 - krev);
-      const f32x2 z = pk2(frev, 1.0f - frev);  // (level k, level k+1) weights
-      f32x2 a = pk2(0.0f, 0.0f), b = pk2(0.0f, 0.0f);
+      if (krev != kcell) {
+        const uint32_t r00 = col * dcol + (m.nz - 2 - krev);
+        f32x2 a = pk2(0.0f, 0.0f), b = pk2(0.0f, 0.0f);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const uint32_t r = r00 + (c & 1 ? drow : 0) + (c & 2 ? dcol : 0);
-        f32x2 t0, t1;
-        asm("ld.global.nc.b64 %0, [%1];" : "=l"(t0) : "l"(m.s0[r].x + 6));
-        const f32x2 wc = mul2(bc2(xy[c]), z);
-        a = fma2(t0, wc, a);
-        if (two) {
+        for (int c = 0; c < 4; ++c) {
+          const uint32_t r = r00 + (c & 1 ? drow : 0) + (c & 2 ? dcol : 0);
+          f32x2 t0, t1;
+          asm("ld.global.nc.b64 %0, [%1];" : "=l"(t0) : "l"(m.s0[r].x + 6));
           asm("ld.global.nc.b64 %0, [%1];" : "=l"(t1) : "l"(m.s1[r].x + 6));
-          b = fma2(t1, wc, b);
+          a = fma2(t0, bc2(xy[c]), a);
+          b = fma2(t1, bc2(xy[c]), b);
         }
+        tz = fma2(w2, sub2(b, a), a);   // w2 = 0 with equal snapshot times (inv_dt = 0)
+        kcell = krev;
       }
-      if (two) a = fma2(w2, sub2(b, a), a);
-      const float temp = sum2(a);
+      // (level k, level k+1) weights (frev, 1 - frev)
+      const float temp = fmaf(lo2(tz), frev, hi2(tz) * (1.0f - frev));
       const double pn = static_cast<double>(
           1000.0f * ex2_approx(static_cast<float>(kInvKappa) * __log2f(temp * inv_theta0)));
       const double dp = pn - p;
