@@ -221,10 +221,18 @@ struct OpsFast {
     // FMA on (T(k), T(k+1)) and the records are not gathered again
     int kcell = -1;
     f32x2 tz = pk2(0.0f, 0.0f);
+    double cx = 0.0;    // lower node and fp32 1/width of the current level cell:
+    float cinv = 0.0f;  // while p stays inside it, no lookup either
 #pragma unroll 1
     for (int it = 0; it < 10 && pending; ++it) {
-      float frev;
-      const int krev = locate_v<G>(m.lev, p, frev, m.levc);
+      float frev = static_cast<float>(p - cx) * cinv;
+      int krev = kcell;
+      if (!(kcell >= 0 && frev > kNodeEps && frev < 1.0f - kNodeEps)) {
+        krev = locate_v<G>(m.lev, p, frev, m.levc);
+        const double2 c = G == 2 ? m.levc[krev] : __ldg(m.lev.cell + krev);
+        cx = c.x;
+        cinv = __int_as_float(static_cast<int>(__double2loint(c.y)));
+      }
       if (krev != kcell) {
         const uint32_t r00 = col * dcol + (m.nz - 2 - krev);
         f32x2 a = pk2(0.0f, 0.0f), b = pk2(0.0f, 0.0f);
