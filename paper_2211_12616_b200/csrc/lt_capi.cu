@@ -93,6 +93,9 @@ struct lt_ctx {
   bool pending = false;          // a box-sort permutation is waiting to be applied
   int64_t pend_start = 0, pend_n = 0;
   uint32_t* sort_buf = nullptr;  // 4 * cap (keys in/out, vals in/out)
+  uint32_t* col_rank = nullptr;  // dense rank of each Morton column code (key compression)
+  int64_t col_rank_n = 0;        // its length (0: not built for the current grid)
+  uint32_t col_count = 0;        // number of columns (nx * ny)
   void* cub_temp = nullptr;
   size_t cub_bytes = 0;
   unsigned long long* counters = nullptr;  // [0] iso_nonconverged, [8, 8 + CK_N) module cycles
@@ -368,6 +371,7 @@ static void free_particles(lt_ctx* c) {
   free_dev(c->ids_alt); c->ids_alt = nullptr;
   c->pending = false;
   free_dev(c->sort_buf); c->sort_buf = nullptr;
+  free_dev(c->col_rank); c->col_rank = nullptr; c->col_rank_n = 0;
   free_dev(c->cub_temp); c->cub_temp = nullptr; c->cub_bytes = 0;
   c->cap = 0;
 }
@@ -608,6 +612,7 @@ int lt_met_grid(lt_ctx* c, int32_t nx, int32_t ny, int32_t nz, const double* lon
   if ((rc = upload_axis(c->ax_lev, asc.data(), nz, c->stream))) return rc;
   const bool same_size = c->nx == nx && c->ny == ny && c->nz == nz && c->prec == precision;
   c->nx = nx; c->ny = ny; c->nz = nz; c->prec = precision;
+  c->col_rank_n = 0;  // the key-compression table belongs to the old grid
   for (auto& s : c->slots) {
     s.valid = false;
     if (!same_size) { free_dev(s.rec); s.rec = nullptr; }
@@ -1382,10 +1387,51 @@ static int sort_typed(lt_ctx* c, int64_t start, int64_t end) {
                             part1by1(static_cast<uint32_t>(c->ny - 1) >> LT_BOX_SHIFT)) *
           box_levels(c->nz) + (box_levels(c->nz) - 1);
   const int morton = c->nx <= 65536 && c->ny <= 65536 && max_morton < (uint64_t(1) << 32);
-  CK(launch_box_keys<Rec>(m, c->lon, c->lat, c->p, start, n, keys_in, vals_in, morton, c->stream));
-  const uint64_t max_key = morton ? max_morton : static_cast<uint64_t>(n_rec(c));
-  int bits = 1;
-  while (bits < 32 && (1ull << bits) <= max_key) ++bits;
+  unsigned int* kzone = reinterpret_cast<unsigned int*>(c->counters + 2);
+  if (morton) {
+    const unsigned int init[2] = {0xFFFFFFFFu, 0u};
+    CK(cudaMemcpyAsync(kzone, init, sizeof init, cudaMemcpyHostToDevice, c->stream));
+  }
+  CK(launch_box_keys<Rec>(m, c->lon, c->lat, c->p, start, n, keys_in, vals_in, morton,
+                          morton ? kzone : nullptr, c->stream));
+  uint64_t max_key = morton ? max_morton : static_cast<uint64_t>(n_rec(c));
+  auto nbits = [](uint64_t v) { int b = 1; while (b < 32 && (1ull << b) <= v) ++b; return b; };
+  if (morton && n > 0) {
+    // the same order in fewer key bits when that saves an 8-bit radix pass:
+    // dense column ranks times the occupied level boxes (compress_keys_kernel)
+    const uint32_t nlev = box_levels(c->nz);
+    const uint64_t ncode = max_morton / nlev + 1;
+    if (c->col_rank_n != static_cast<int64_t>(ncode)) {
+      std::vector<uint32_t> rank(ncode, 0u);
+      std::vector<unsigned char> used(ncode, 0);
+      for (int i = 0; i < c->nx; ++i)
+        for (int j = 0; j < c->ny; ++j)
+          used[(part1by1(static_cast<uint32_t>(i) >> LT_BOX_SHIFT) << 1) |
+               part1by1(static_cast<uint32_t>(j) >> LT_BOX_SHIFT)] = 1;
+      uint32_t r = 0;
+      for (uint64_t code = 0; code < ncode; ++code) {
+        rank[code] = r;
+        r += used[code];
+      }
+      free_dev(c->col_rank);
+      c->col_rank = nullptr;
+      if (int rc = alloc_dev(reinterpret_cast<void**>(&c->col_rank), sizeof(uint32_t) * ncode, "column ranks"))
+        return rc;
+      CK(cudaMemcpy(c->col_rank, rank.data(), sizeof(uint32_t) * ncode, cudaMemcpyHostToDevice));
+      c->col_rank_n = static_cast<int64_t>(ncode);
+      c->col_count = r;
+    }
+    unsigned int zone[2];
+    CK(cudaMemcpyAsync(zone, kzone, sizeof zone, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    const uint32_t nocc = zone[1] - zone[0] + 1;
+    const uint64_t max_c = static_cast<uint64_t>(c->col_count) * nocc - 1;
+    if ((nbits(max_c) + 7) / 8 < (nbits(max_key) + 7) / 8) {
+      CK(launch_compress_keys(keys_in, n, c->col_rank, nlev, zone[0], nocc, c->stream));
+      max_key = max_c;
+    }
+  }
+  const int bits = nbits(max_key);
   size_t need = 0;
   CK(sort_pairs(nullptr, need, keys_in, keys_out, vals_in, vals_out, n, bits, c->stream));
   if (need > c->cub_bytes) {

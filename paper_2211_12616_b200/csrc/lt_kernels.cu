@@ -80,10 +80,13 @@ __global__ void rng_fill_kernel(int mode, uint64_t seed_or_state, int64_t step, 
 // so the keys — and the stable sort's permutation — are the oracle's
 // box_keys, at a fraction of the fp64 bracketing's cost.  G = 2 on a
 // geographic grid (computed lon/lat cells, log-guessed levels), 1 elsewhere.
+// kzone[0] / kzone[1] collect the smallest and largest level box (the
+// occupied level range, for compress_keys_kernel)
 template <class Rec, int G>
 __global__ void box_key_kernel(const __grid_constant__ MetView<Rec> m, const double* lon, const double* lat,
                                const double* p, int64_t start, int64_t n, uint32_t* keys,
-                               uint32_t* vals, int morton) {
+                               uint32_t* vals, int morton, unsigned int* kzone) {
+  uint32_t kmin = 0xFFFFFFFFu, kmax = 0u;
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t s = start + t;
@@ -94,6 +97,33 @@ __global__ void box_key_kernel(const __grid_constant__ MetView<Rec> m, const dou
     const uint32_t r00 = (static_cast<uint32_t>(i) * m.ny + j) * (m.nz - 1) + k;
     keys[t] = morton ? box_key_morton(i, j, k, m.nz) : r00;
     vals[t] = static_cast<uint32_t>(t);
+    const uint32_t kb = static_cast<uint32_t>(k) / LT_BOX_ZDIV;
+    kmin = min(kmin, kb);
+    kmax = max(kmax, kb);
+  }
+  if (kzone) {
+    kmin = __reduce_min_sync(0xffffffffu, kmin);
+    kmax = __reduce_max_sync(0xffffffffu, kmax);
+    if ((threadIdx.x & 31) == 0) {
+      atomicMin(kzone, kmin);
+      atomicMax(kzone + 1, kmax);
+    }
+  }
+}
+
+// The same order with fewer key bits: Morton column codes are sparse (0.25
+// deg: 2.5e6 codes for 1.04e6 columns) and most level boxes hold no
+// particle, so key = column * nlev + kb becomes rank[column] * nocc +
+// (kb - kmin) — strictly monotone on the keys present, hence the same
+// stable permutation, in 24 bits instead of 28 at cfg3 (three onesweep
+// passes instead of four)
+__global__ void compress_keys_kernel(uint32_t* keys, int64_t n, const uint32_t* __restrict__ rank,
+                                     uint32_t nlev, uint32_t kmin, uint32_t nocc) {
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t key = keys[t];
+    const uint32_t col = key / nlev;
+    keys[t] = __ldg(rank + col) * nocc + (key - col * nlev - kmin);
   }
 }
 
@@ -252,15 +282,22 @@ cudaError_t launch_philox_kat(const uint32_t* ctr, const uint32_t* key, uint32_t
 template <class Rec>
 cudaError_t launch_box_keys(const MetView<Rec>& m, const double* lon, const double* lat,
                             const double* p, int64_t start, int64_t n, uint32_t* keys,
-                            uint32_t* vals, int morton, cudaStream_t st) {
+                            uint32_t* vals, int morton, unsigned int* kzone, cudaStream_t st) {
   const bool geo = m.lon.uniform && m.lat.uniform && !m.lev.uniform && m.lev.logscale &&
                    m.lev.n - 1 <= kLevCap;
-  if (geo) box_key_kernel<Rec, 2><<<grid_for(n), 256, 0, st>>>(m, lon, lat, p, start, n, keys, vals, morton);
-  else box_key_kernel<Rec, 1><<<grid_for(n), 256, 0, st>>>(m, lon, lat, p, start, n, keys, vals, morton);
+  if (geo) box_key_kernel<Rec, 2><<<grid_for(n), 256, 0, st>>>(m, lon, lat, p, start, n, keys, vals, morton, kzone);
+  else box_key_kernel<Rec, 1><<<grid_for(n), 256, 0, st>>>(m, lon, lat, p, start, n, keys, vals, morton, kzone);
   return cudaGetLastError();
 }
-template cudaError_t launch_box_keys<RecF>(const MetView<RecF>&, const double*, const double*, const double*, int64_t, int64_t, uint32_t*, uint32_t*, int, cudaStream_t);
-template cudaError_t launch_box_keys<RecD>(const MetView<RecD>&, const double*, const double*, const double*, int64_t, int64_t, uint32_t*, uint32_t*, int, cudaStream_t);
+
+cudaError_t launch_compress_keys(uint32_t* keys, int64_t n, const uint32_t* rank, uint32_t nlev,
+                                 uint32_t kmin, uint32_t nocc, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  compress_keys_kernel<<<grid_for(n), 256, 0, st>>>(keys, n, rank, nlev, kmin, nocc);
+  return cudaGetLastError();
+}
+template cudaError_t launch_box_keys<RecF>(const MetView<RecF>&, const double*, const double*, const double*, int64_t, int64_t, uint32_t*, uint32_t*, int, unsigned int*, cudaStream_t);
+template cudaError_t launch_box_keys<RecD>(const MetView<RecD>&, const double*, const double*, const double*, int64_t, int64_t, uint32_t*, uint32_t*, int, unsigned int*, cudaStream_t);
 
 template <class T>
 cudaError_t launch_permute(T* dst, const T* src, const uint32_t* perm, int64_t start, int64_t n,

@@ -59,7 +59,9 @@ __host__ __device__ inline uint32_t box_key_morton(int i, int j, int k, int nz) 
 template <class Rec>
 cudaError_t launch_box_keys(const MetView<Rec>& m, const double* lon, const double* lat,
                             const double* p, int64_t start, int64_t n, uint32_t* keys,
-                            uint32_t* vals, int morton, cudaStream_t st);
+                            uint32_t* vals, int morton, unsigned int* kzone, cudaStream_t st);
+cudaError_t launch_compress_keys(uint32_t* keys, int64_t n, const uint32_t* rank, uint32_t nlev,
+                                 uint32_t kmin, uint32_t nocc, cudaStream_t st);
 constexpr int kRowSet = 4;
 struct RowSet {
   const double* src[kRowSet];
