@@ -995,6 +995,8 @@ static int run_typed(lt_ctx* c, const lt_control* ctl, uint32_t modules, int64_t
     k.meso_amp = std::sqrt(1.0 - rr);
     k.decay = ctl->decay_tau > 0.0 ? std::exp(-dt / ctl->decay_tau) : 1.0;
     k.conv_scale = ctl->conv_prob != 0.0 ? (ctl->p_surf - ctl->conv_p_top) / ctl->conv_prob : 0.0;
+    philox_round_keys(static_cast<uint32_t>(ctl->rng_seed_global),
+                      static_cast<uint32_t>(ctl->rng_seed_global >> 32), k.philox_rk);
   }
   const bool need_met = modules & (M_ADVECTION | M_TURB | M_MESO | M_SEDI | M_ISOSURF | M_METEO |
                                    M_ISOSURF_INIT);

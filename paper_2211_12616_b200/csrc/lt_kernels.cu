@@ -267,7 +267,13 @@ cudaError_t launch_rng_fill(int mode, uint64_t seed, int64_t step, int64_t start
 // pairs: the known-answer hook for Philox4x32-10 (Random123's kat_vectors)
 __global__ void philox_kat_kernel(const uint4* ctr, const uint2* key, uint4* out, int n) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = philox(ctr[i], key[i]);
+  if (i >= n) return;
+  // both forms of the block function: a disagreement poisons the answer
+  uint32_t rk[20];
+  philox_round_keys(key[i].x, key[i].y, rk);
+  const uint4 a = philox(ctr[i], key[i]), b = philox_rk(ctr[i], rk);
+  const bool same = a.x == b.x && a.y == b.y && a.z == b.z && a.w == b.w;
+  out[i] = same ? a : make_uint4(~a.x, ~a.y, ~a.z, ~a.w);
 }
 
 cudaError_t launch_philox_kat(const uint32_t* ctr, const uint32_t* key, uint32_t* out, int n,

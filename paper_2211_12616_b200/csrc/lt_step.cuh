@@ -25,6 +25,7 @@ struct StepConst {
   double meso_amp;  // sqrt(1 - r^2)
   double decay;     // exp(-dt / decay_tau) (host libm; 1 when decay is off)
   double conv_scale;  // (p_surf - conv_p_top) / conv_prob (fast path only)
+  uint32_t philox_rk[20];  // Philox round keys of ctl.rng_seed_global (lt_device.cuh)
 };
 
 template <class Rec>
@@ -251,7 +252,7 @@ struct OpsFast {
       // (level k, level k+1) weights (frev, 1 - frev)
       const float temp = fmaf(lo2(tz), frev, hi2(tz) * (1.0f - frev));
       const double pn = static_cast<double>(
-          1000.0f * ex2_approx(static_cast<float>(kInvKappa) * __log2f(temp * inv_theta0)));
+          1000.0f * ex2_approx(static_cast<float>(kInvKappa) * lg2_approx(temp * inv_theta0)));
       const double dp = pn - p;
       p = pn;
       pending = fabs(dp) >= 0.1;
@@ -277,7 +278,7 @@ struct OpsFast {
     corner_std_pairs(q, sig);
   }
   __device__ static double power(double x, double e) {
-    return static_cast<double>(ex2_approx(static_cast<float>(e) * __log2f(static_cast<float>(x))));
+    return static_cast<double>(ex2_approx(static_cast<float>(e) * lg2_approx(static_cast<float>(x))));
   }
   __device__ static void normals(uint64_t seed, int64_t step, uint64_t gid, int stream, double z[3]) {
     counter_normals_fast(seed, step, gid, stream, z);
@@ -300,7 +301,7 @@ __device__ __forceinline__ void draws(const StepArgs<Rec>& a, int64_t s, uint64_
     return;
   }
   if (RM == RNG_PHILOX) {
-    philox_stream(ctl.rng_seed_global, step, gid, stream, x);
+    philox_stream(a.kc.philox_rk, step, gid, stream, x);
     return;
   }
   if (RM == RNG_FAITHFUL) {
@@ -322,7 +323,7 @@ __device__ __forceinline__ void draws(const StepArgs<Rec>& a, int64_t s, uint64_
   } else if (ctl.rng_mode == RNG_FAITHFUL) {
     faithful_stream(a.faithful_state, gid - static_cast<uint64_t>(a.faithful_base), stream, x);
   } else {
-    philox_stream(ctl.rng_seed_global, step, gid, stream, x);
+    philox_stream(a.kc.philox_rk, step, gid, stream, x);
   }
 }
 
@@ -449,7 +450,7 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, FAST ? LT_STEP_MIN_BLOCKS : LT_
 #ifdef LT_PROBE_NO_RNG  // timing probe only: what the draws cost
           for (int q = 0; q < 6; ++q) early[q] = 0.25f * static_cast<float>((gid >> q) & 3) - 0.3f;
 #else
-          philox_normals_fast(ctl.rng_seed_global, stp, gid, early);
+          philox_normals_fast(a.kc.philox_rk, stp, gid, early);
 #endif
         } else {
           double z[3];
@@ -506,7 +507,7 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, FAST ? LT_STEP_MIN_BLOCKS : LT_
       double zturb[3] = {0.0, 0.0, 0.0}, zmeso[3] = {0.0, 0.0, 0.0};
       if (kBoth && (want_turb || want_meso) && act) {
         if (RM == RNG_PHILOX) {
-          philox_turb_meso(ctl.rng_seed_global, stp, gid, zturb, zmeso);
+          philox_turb_meso(a.kc.philox_rk, stp, gid, zturb, zmeso);
         } else {
 #pragma unroll 1
           for (int st = 1; st <= 2; ++st) {
