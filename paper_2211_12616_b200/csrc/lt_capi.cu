@@ -433,6 +433,9 @@ int lt_particles_alloc(lt_ctx* c, int64_t capacity, int32_t nq, int32_t with_bat
   int rc = check_ctx(c);
   if (rc) return rc;
   if (capacity < 0) return fail(LT_ERR_ARG, "capacity %lld < 0", (long long)capacity);
+  // particle ids and the kernels' slot arithmetic are 32-bit (2^31 particles
+  // would need > 180 GB of state alone)
+  if (capacity > INT32_MAX) return fail(LT_ERR_ARG, "capacity %lld > 2^31 - 1", (long long)capacity);
   if (nq < 5) return fail(LT_ERR_ARG, "nq >= 5 violated (meteo sampling needs slots 0..4)");
   CK(cudaStreamSynchronize(c->stream));
   free_particles(c);

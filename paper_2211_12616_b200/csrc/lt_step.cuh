@@ -88,10 +88,22 @@ __device__ __forceinline__ void st_state(double* p, double v) { *p = v; }
 #ifndef LT_STEP_MIN_BLOCKS
 #define LT_STEP_MIN_BLOCKS (1024 / LT_STEP_BLOCK)
 #endif
-// resident blocks per SM the exact (FAST = 0) kernels are compiled for
+// resident blocks per SM the exact (FAST = 0) kernels are compiled for: 4
+// (64 registers), except the adv+turb+meso chain with in-kernel Philox draws,
+// whose fp64 Box-Muller pairs spill less at 3 blocks (80 registers): -3.2 %
+// at cfg3, where the counter-word and full-chain kernels measured +0.7 % and
+// +5 % slower at 3
 #ifndef LT_EXACT_MIN_BLOCKS
-#define LT_EXACT_MIN_BLOCKS LT_STEP_MIN_BLOCKS
+#define LT_EXACT_MIN_BLOCKS 4
 #endif
+#ifndef LT_EXACT_PHILOX_MIN_BLOCKS
+#define LT_EXACT_PHILOX_MIN_BLOCKS 3
+#endif
+constexpr int step_min_blocks(uint32_t fixed, int fast, int rm) {
+  return fast ? LT_STEP_MIN_BLOCKS
+              : (fixed == (M_TIMESTEPS | M_ADVECTION | M_TURB | M_MESO | M_POSITION) && rm == RNG_PHILOX
+                     ? LT_EXACT_PHILOX_MIN_BLOCKS : LT_EXACT_MIN_BLOCKS);
+}
 
 // Arithmetic policy: FAST = 0 reproduces numpy's operation sequence in
 // fp64; FAST = 1 is the mixed-precision path of lt_device.cuh (fp32 store
@@ -338,7 +350,7 @@ __device__ __forceinline__ int64_t row_index(const StepArgs<Rec>& a, int64_t s, 
 // PM: 0 one step, 1 one step applying a pending permutation (PERM), 2
 // a.nsteps steps per particle (MULTI)
 template <class Rec, uint32_t FIXED, int FAST, int RM, int PM>
-__global__ void __launch_bounds__(LT_STEP_BLOCK, FAST ? LT_STEP_MIN_BLOCKS : LT_EXACT_MIN_BLOCKS)
+__global__ void __launch_bounds__(LT_STEP_BLOCK, step_min_blocks(FIXED, FAST, RM))
     step_kernel(const __grid_constant__ StepArgs<Rec> a) {
   using O = Ops<Rec, FAST>;
   constexpr bool PERM = PM == 1, MULTI = PM == 2;
