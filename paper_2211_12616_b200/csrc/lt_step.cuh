@@ -362,7 +362,12 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, step_min_blocks(FIXED, FAST, RM
   const int64_t per = (ntile + gridDim.x - 1) / gridDim.x;
   const int64_t s_lo = a.start + static_cast<int64_t>(blockIdx.x) * per * blockDim.x;
   const int64_t s_hi = min(a.end, s_lo + per * blockDim.x);
-  const int64_t stride = blockDim.x;
+  // 32-bit slots in the loop (capacity < 2^31, lt_particles_alloc): every
+  // row address is one IMAD.WIDE.U32 on the kernel-parameter base instead
+  // of a 64-bit add pair
+  const uint32_t lo32 = static_cast<uint32_t>(min(s_lo, s_hi)), hi32 = static_cast<uint32_t>(s_hi);
+  const uint32_t stride = blockDim.x;
+  const uint32_t pstart = static_cast<uint32_t>(a.perm_start);
   unsigned long long nonconv = 0;
 
   // per-launch switches, decided once outside the particle loop
@@ -391,15 +396,15 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, step_min_blocks(FIXED, FAST, RM
   const bool want_conv = (mods & M_CONVECTION) && ctl.conv_prob != 0.0;
   const bool turb_h = ctl.turb_dx > 0.0, turb_v = ctl.turb_dz > 0.0;
 
-  for (int64_t s = s_lo + threadIdx.x; s < s_hi; s += stride) {
+  for (uint32_t s = lo32 + threadIdx.x; s < hi32; s += stride) {
     // PERM: this slot's particle comes from old slot `src` (box sort applied
     // on the fly: gathered reads, coalesced writes to the o_* rows)
-    const int64_t src = PERM ? a.perm_start + a.perm[s - a.perm_start] : s;
+    const uint32_t src = PERM ? pstart + a.perm[s - pstart] : s;
     // stage the next particle's state rows into L2 while this one runs
     // (costs no registers; the loads below then hit L2 instead of HBM)
 #ifndef LT_NO_PREFETCH
-    if (!PERM && s + stride < s_hi) {
-      const int64_t nx = s + stride;
+    if (!PERM && s + stride < hi32) {
+      const uint32_t nx = s + stride;
       prefetch_l2(a.time + nx); prefetch_l2(a.lon + nx); prefetch_l2(a.lat + nx);
       prefetch_l2(a.p + nx);
       if (mods & M_MESO) {
@@ -407,8 +412,8 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, step_min_blocks(FIXED, FAST, RM
       }
       if (a.ids && (mods & (M_TURB | M_MESO | M_CONVECTION))) prefetch_l2(a.ids + nx);
     }
-    if (PERM && s + stride < s_hi) {  // the next tile's gathered source rows
-      const int64_t nx = a.perm_start + a.perm[s + stride - a.perm_start];
+    if (PERM && s + stride < hi32) {  // the next tile's gathered source rows
+      const uint32_t nx = pstart + a.perm[s + stride - pstart];
       prefetch_l2(a.time + nx); prefetch_l2(a.lon + nx); prefetch_l2(a.lat + nx);
       prefetch_l2(a.p + nx);
       prefetch_l2(a.uvwp[0] + nx); prefetch_l2(a.uvwp[1] + nx); prefetch_l2(a.uvwp[2] + nx);
