@@ -206,6 +206,7 @@ Axis view(const AxisHost& a) {
   v.lo = a.lo;
   v.hi = a.hi;
   v.n = a.n;
+  v.nm2 = a.n - 2;
   v.logscale = a.logscale;
   v.g0 = a.g0;
   v.ginv = a.ginv;
