@@ -106,6 +106,10 @@ struct lt_ctx {
   AxisHost ax_lon, ax_lat, ax_lev;
   Slot slots[3];
   int use0 = -1, use1 = -1;
+  // per-cell mesoscale spreads of slot sig_slot (MetView::sig0), built on
+  // the compute stream before the first meso launch on a new met0
+  double* sig_tab = nullptr;
+  int sig_slot = -1;
   void* staging = nullptr;
   size_t staging_bytes = 0;
   cudaEvent_t staging_free = nullptr;
@@ -232,6 +236,7 @@ MetView<Rec> met_view(const lt_ctx* c) {
   m.t0 = c->slots[c->use0].t_met;
   m.t1 = c->slots[c->use1].t_met;
   m.inv_dt = m.t1 != m.t0 ? 1.0 / (m.t1 - m.t0) : 0.0;
+  m.sig0 = nullptr;
   const int ncell = c->ax_lev.n - 1;
   if (ncell <= kLevCap) std::memcpy(m.levc, c->ax_lev.host_cell.data(), sizeof(double2) * ncell);
   return m;
@@ -373,6 +378,7 @@ static void free_particles(lt_ctx* c) {
   c->pending = false;
   free_dev(c->sort_buf); c->sort_buf = nullptr;
   free_dev(c->col_rank); c->col_rank = nullptr; c->col_rank_n = 0;
+  free_dev(c->sig_tab); c->sig_tab = nullptr; c->sig_slot = -1;
   free_dev(c->cub_temp); c->cub_temp = nullptr; c->cub_bytes = 0;
   c->cap = 0;
 }
@@ -617,6 +623,9 @@ int lt_met_grid(lt_ctx* c, int32_t nx, int32_t ny, int32_t nz, const double* lon
   const bool same_size = c->nx == nx && c->ny == ny && c->nz == nz && c->prec == precision;
   c->nx = nx; c->ny = ny; c->nz = nz; c->prec = precision;
   c->col_rank_n = 0;  // the key-compression table belongs to the old grid
+  free_dev(c->sig_tab);  // so does the spread table
+  c->sig_tab = nullptr;
+  c->sig_slot = -1;
   for (auto& s : c->slots) {
     s.valid = false;
     if (!same_size) { free_dev(s.rec); s.rec = nullptr; }
@@ -629,6 +638,7 @@ static int met_prepare(lt_ctx* c, int slot) {
   if (!c->nx) return fail(LT_ERR_STATE, "met grid not set");
   if (slot < 0 || slot > 2) return fail(LT_ERR_ARG, "met slot %d outside [0, 3)", slot);
   Slot& s = c->slots[slot];
+  if (c->sig_slot == slot) c->sig_slot = -1;  // its spread table goes stale
   // never overwrite a slot the compute stream may still be reading: the copy
   // stream waits (on the device) for the compute work issued so far
   if (c->marked) CK(cudaStreamWaitEvent(c->copy, c->compute_mark, 0));
@@ -1007,6 +1017,19 @@ static int run_typed(lt_ctx* c, const lt_control* ctl, uint32_t modules, int64_t
   if (need_met) {
     if (c->use0 < 0) return fail(LT_ERR_STATE, "no met snapshots selected (lt_met_use)");
     a.met = met_view<Rec>(c);
+    if ((modules & M_MESO) && ctl->turb_meso != 0.0) {
+      // the mesoscale spreads of met0, once per met0 snapshot
+      if (!c->sig_tab) {
+        if (int rc = alloc_dev(reinterpret_cast<void**>(&c->sig_tab), 4 * sizeof(double) * n_rec(c), "spread table"))
+          return rc;
+        c->sig_slot = -1;
+      }
+      if (c->sig_slot != c->use0) {
+        CK(launch_spread_table<Rec>(a.met, c->nx, c->sig_tab, c->stream));
+        c->sig_slot = c->use0;
+      }
+      a.met.sig0 = c->sig_tab;
+    }
   } else {
     std::memset(&a.met, 0, sizeof(a.met));
   }

@@ -75,6 +75,32 @@ __global__ void rng_fill_kernel(int mode, uint64_t seed_or_state, int64_t step, 
   }
 }
 
+// The mesoscale spreads of every met0 cell (sigma_u, sigma_v, sigma_w of
+// its eight corners, physics.py:168-176) with the exact kernels' own code
+// (gather + corner_std, numpy's pairwise order in fp64): the step kernels
+// then read one 32-byte entry per particle instead of gathering the four
+// corner records and reducing them.  Identical values, computed once per
+// met0 snapshot instead of once per particle and step.  Cells on the last
+// lon/lat row are never a corner-000 cell (locate clips to n - 2): zeros.
+template <class Rec>
+__global__ void spread_table_kernel(const __grid_constant__ MetView<Rec> m, int nx, double4* out) {
+  const uint32_t dcol = static_cast<uint32_t>(m.nz - 1);
+  const uint32_t nrec = static_cast<uint32_t>(nx) * m.ny * dcol;
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < nrec; r += gridDim.x * blockDim.x) {
+    const uint32_t col = r / dcol;
+    const uint32_t i = col / m.ny, j = col - i * m.ny;
+    double4 o = make_double4(0.0, 0.0, 0.0, 0.0);
+    if (i + 1 < static_cast<uint32_t>(nx) && j + 1 < static_cast<uint32_t>(m.ny)) {
+      Corners<Rec> q;
+      gather(m.s0, m, r, q, 7);
+      o.x = corner_std(q, 0);
+      o.y = corner_std(q, 1);
+      o.z = corner_std(q, 2);
+    }
+    out[r] = o;
+  }
+}
+
 // Box keys from the fast kernels' cell lookup: it returns searchsorted's
 // cells bit for bit (near-node guesses are settled exactly, lt_device.cuh),
 // so the keys — and the stable sort's permutation — are the oracle's
@@ -231,6 +257,16 @@ static int grid_for(int64_t n, int block = 256) {
   if (g > 148 * 64) g = 148 * 64;
   return static_cast<int>(g);
 }
+
+template <class Rec>
+cudaError_t launch_spread_table(const MetView<Rec>& m, int nx, double* out, cudaStream_t st) {
+  const int64_t n = static_cast<int64_t>(nx) * m.ny * (m.nz - 1);
+  spread_table_kernel<Rec><<<grid_for(n), 256, 0, st>>>(m, nx, reinterpret_cast<double4*>(out));
+  return cudaGetLastError();
+}
+template cudaError_t launch_spread_table<RecF>(const MetView<RecF>&, int, double*, cudaStream_t);
+template cudaError_t launch_spread_table<RecD>(const MetView<RecD>&, int, double*, cudaStream_t);
+
 
 template <class Src, class Rec>
 cudaError_t launch_pack_fields(Rec* out, const Src* u, const Src* v, const Src* w, const Src* T,

@@ -25,6 +25,9 @@ cudaError_t launch_pack_fields(Rec* out, const Src* u, const Src* v, const Src* 
 template <class Rec>
 cudaError_t launch_pack_nodes(Rec* out, const float4* nodes, int nx, int ny, int nz, int nx_src,
                               cudaStream_t st);
+// per-cell mesoscale spreads of the met0 records (MetView::sig0)
+template <class Rec>
+cudaError_t launch_spread_table(const MetView<Rec>& m, int nx, double* out, cudaStream_t st);
 cudaError_t launch_rng_fill(int mode, uint64_t seed, int64_t step, int64_t start, int64_t end,
                             const uint32_t* ids, double* conv, double* turb, double* meso,
                             cudaStream_t st);

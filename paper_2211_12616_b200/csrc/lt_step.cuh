@@ -168,11 +168,9 @@ struct Ops {
     return col * (m.nz - 1) + (m.nz - 2 - locate(m.lev, p, frev));
   }
   // corner spreads of u, v, w in met0 around record r00 (meso diffusion)
+  // (run_typed builds the table of met0 before any launch with meso)
   __device__ static void spreads(const MetView<Rec>& m, uint32_t r00, double sig[3]) {
-    Corners<Rec> q;
-    gather(m.s0, m, r00, q, 7);
-#pragma unroll
-    for (int f = 0; f < 3; ++f) sig[f] = corner_std(q, f);
+    load_spreads(m.sig0, r00, sig);
   }
   // x^e (isosurface potential temperature, physics.py:233-234, 256-257)
   __device__ static double power(double x, double e) { return pow(x, e); }
@@ -285,9 +283,7 @@ struct OpsFast {
     return col * (m.nz - 1) + (m.nz - 2 - locate_v<G>(m.lev, p, frev, m.levc));
   }
   __device__ static void spreads(const MetView<RecF>& m, uint32_t r00, double sig[3]) {
-    PairsF q;
-    gather_pairs(m.s0, m, r00, q, 7);
-    corner_std_pairs(q, sig);
+    load_spreads(m.sig0, r00, sig);
   }
   __device__ static double power(double x, double e) {
     return static_cast<double>(ex2_approx(static_cast<float>(e) * lg2_approx(static_cast<float>(x))));
