@@ -141,6 +141,12 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            # nvidia-smi takes a while to start: begin the timed region only
+            # once it is sampling, so short regions are covered too
+            t0 = time.time()
+            while not self.rows and self.proc.poll() is None and time.time() - t0 < 5.0:
+                time.sleep(0.01)
+            self.rows.clear()
         except OSError:
             self.proc = None
         return self
@@ -153,7 +159,11 @@ class ClockSampler:
 
     def __exit__(self, *exc):
         if self.proc:
-            time.sleep(0.15)
+            # at least one sample taken during (or right at the end of) the region
+            t0 = time.time()
+            while not self.rows and self.proc.poll() is None and time.time() - t0 < 2.0:
+                time.sleep(0.01)
+            time.sleep(0.05)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=2)
