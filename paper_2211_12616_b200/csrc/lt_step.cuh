@@ -71,6 +71,9 @@ struct StepArgs {
 __device__ __forceinline__ void prefetch_l2(const void* ptr) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
 }
+__device__ __forceinline__ void prefetch_l1(const void* ptr) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(ptr));
+}
 
 // particle-state rows are touched once per step: stream them past L1
 // (evict-first) so L1 keeps the met records the gathers reuse
@@ -414,6 +417,14 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, step_min_blocks(FIXED, FAST, RM
       prefetch_l2(a.p + nx);
       prefetch_l2(a.uvwp[0] + nx); prefetch_l2(a.uvwp[1] + nx); prefetch_l2(a.uvwp[2] + nx);
       prefetch_l2(a.ids + nx);
+    }
+#endif
+#ifndef LT_NO_L1PF_UVWP
+    // exact kernels: this particle's AR(1) state into L1 now, so the meso
+    // step's loads of it (issued late, after the gathers) hit L1 (-0.5 %;
+    // the fast kernels measured +2.6 % with it — their L1 holds the records)
+    if (FAST == 0 && (mods & M_MESO)) {
+      prefetch_l1(a.uvwp[0] + src); prefetch_l1(a.uvwp[1] + src); prefetch_l1(a.uvwp[2] + src);
     }
 #endif
     if (FIXED == 0 && clocks) t_last = clock64();
