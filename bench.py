@@ -860,6 +860,12 @@ def main():
     e2e_drv = None
     if ws == 1 and args.e2e_steps > 0 and stream is None and wl == "cfg3":
         eng.close()   # the driver builds its own device image
+        # and its own pinned host ensemble: release the e2e leg's first
+        # (a process holding both measured cudaFree-bound region deletes
+        # of 0.03-1.5 s inside the driver's wall clock)
+        import gc
+        hens = hcache = None
+        gc.collect()
         e2e_drv = e2e_driver_run(wl)
 
     cpu = None

@@ -106,10 +106,14 @@ struct lt_ctx {
   AxisHost ax_lon, ax_lat, ax_lev;
   Slot slots[3];
   int use0 = -1, use1 = -1;
-  // per-cell mesoscale spreads of slot sig_slot (MetView::sig0), built on
-  // the compute stream before the first meso launch on a new met0
-  double* sig_tab = nullptr;
-  int sig_slot = -1;
+  // per-cell mesoscale spreads (MetView::sig0): two tables tagged with the
+  // met slot they describe — met0's, and met1's, prebuilt on the copy stream
+  // while the steps run, so a rotation finds its new met0's table ready
+  double* sig_buf[2] = {nullptr, nullptr};
+  int sig_of[2] = {-1, -1};
+  cudaEvent_t sig_ready[2] = {nullptr, nullptr};
+  cudaEvent_t sig_mark = nullptr;  // compute work that may still read a table
+  bool meso_seen = false;          // prebuild met1's table only once meso has run
   void* staging = nullptr;
   size_t staging_bytes = 0;
   cudaEvent_t staging_free = nullptr;
@@ -355,6 +359,8 @@ static int ctx_init(lt_ctx* c) {
   CK(cudaEventCreateWithFlags(&c->staging_free, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->compute_mark, cudaEventDisableTiming));
   for (auto& s : c->slots) CK(cudaEventCreateWithFlags(&s.ready, cudaEventDisableTiming));
+  for (auto& e : c->sig_ready) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->sig_mark, cudaEventDisableTiming));
   int rc = alloc_dev(reinterpret_cast<void**>(&c->counters), 32 * sizeof(unsigned long long), "counters");
   if (rc) return rc;
   rc = alloc_dev(reinterpret_cast<void**>(&c->bad), sizeof(int), "flag");
@@ -378,7 +384,6 @@ static void free_particles(lt_ctx* c) {
   c->pending = false;
   free_dev(c->sort_buf); c->sort_buf = nullptr;
   free_dev(c->col_rank); c->col_rank = nullptr; c->col_rank_n = 0;
-  free_dev(c->sig_tab); c->sig_tab = nullptr; c->sig_slot = -1;
   free_dev(c->cub_temp); c->cub_temp = nullptr; c->cub_bytes = 0;
   c->cap = 0;
 }
@@ -408,6 +413,11 @@ int lt_ctx_destroy(lt_ctx* c) {
   cudaEventDestroy(c->ev_stop);
   cudaEventDestroy(c->staging_free);
   cudaEventDestroy(c->compute_mark);
+  for (int b = 0; b < 2; ++b) {
+    free_dev(c->sig_buf[b]);
+    cudaEventDestroy(c->sig_ready[b]);
+  }
+  cudaEventDestroy(c->sig_mark);
   cudaStreamDestroy(c->stream);
   cudaStreamDestroy(c->copy);
   cudaStreamDestroy(c->d2h);
@@ -623,9 +633,11 @@ int lt_met_grid(lt_ctx* c, int32_t nx, int32_t ny, int32_t nz, const double* lon
   const bool same_size = c->nx == nx && c->ny == ny && c->nz == nz && c->prec == precision;
   c->nx = nx; c->ny = ny; c->nz = nz; c->prec = precision;
   c->col_rank_n = 0;  // the key-compression table belongs to the old grid
-  free_dev(c->sig_tab);  // so does the spread table
-  c->sig_tab = nullptr;
-  c->sig_slot = -1;
+  for (int b = 0; b < 2; ++b) {  // so do the spread tables
+    free_dev(c->sig_buf[b]);
+    c->sig_buf[b] = nullptr;
+    c->sig_of[b] = -1;
+  }
   for (auto& s : c->slots) {
     s.valid = false;
     if (!same_size) { free_dev(s.rec); s.rec = nullptr; }
@@ -638,7 +650,8 @@ static int met_prepare(lt_ctx* c, int slot) {
   if (!c->nx) return fail(LT_ERR_STATE, "met grid not set");
   if (slot < 0 || slot > 2) return fail(LT_ERR_ARG, "met slot %d outside [0, 3)", slot);
   Slot& s = c->slots[slot];
-  if (c->sig_slot == slot) c->sig_slot = -1;  // its spread table goes stale
+  for (int& t : c->sig_of)
+    if (t == slot) t = -1;  // its spread table goes stale
   // never overwrite a slot the compute stream may still be reading: the copy
   // stream waits (on the device) for the compute work issued so far
   if (c->marked) CK(cudaStreamWaitEvent(c->copy, c->compute_mark, 0));
@@ -959,6 +972,40 @@ int lt_clim_load(lt_ctx* c, int32_t nlat, int32_t np_, const double* lat_grid,
 // ------------------------------------------------------------------ compute
 
 extern "C++" {
+// The spread table of met slot `slot`: an existing one, or built into the
+// buffer that describes neither met0 nor met1 — on the compute stream (after
+// any prebuild still writing that buffer), or on the copy stream (after the
+// slot's packing and after every compute launch issued so far, which may
+// still read the buffer's previous table)
+template <class Rec>
+static int spread_table_for(lt_ctx* c, int slot, bool on_copy, int* idx) {
+  for (int b = 0; b < 2; ++b)
+    if (c->sig_of[b] == slot) { *idx = b; return LT_OK; }
+  int b = 0;
+  while (b < 2 && (c->sig_of[b] == c->use0 || c->sig_of[b] == c->use1) && c->sig_of[b] >= 0) ++b;
+  if (b == 2) return fail(LT_ERR_STATE, "no free spread table (slots %d/%d)", c->use0, c->use1);
+  if (!c->sig_buf[b]) {
+    if (int rc = alloc_dev(reinterpret_cast<void**>(&c->sig_buf[b]), 4 * sizeof(double) * n_rec(c), "spread table"))
+      return rc;
+  }
+  MetView<Rec> m = met_view<Rec>(c);
+  m.s0 = static_cast<const Rec*>(c->slots[slot].rec);
+  cudaStream_t st = c->stream;
+  if (on_copy) {
+    st = c->copy;
+    CK(cudaEventRecord(c->sig_mark, c->stream));
+    CK(cudaStreamWaitEvent(c->copy, c->sig_mark, 0));
+    CK(cudaStreamWaitEvent(c->copy, c->slots[slot].ready, 0));
+  } else {
+    CK(cudaStreamWaitEvent(c->stream, c->sig_ready[b], 0));
+  }
+  CK(launch_spread_table<Rec>(m, c->nx, c->sig_buf[b], st));
+  CK(cudaEventRecord(c->sig_ready[b], st));
+  c->sig_of[b] = slot;
+  *idx = b;
+  return LT_OK;
+}
+
 template <class Rec>
 static int run_typed(lt_ctx* c, const lt_control* ctl, uint32_t modules, int64_t start,
                      int64_t end, int64_t step, uint64_t fstate, int64_t fbase, uint32_t flags,
@@ -1018,17 +1065,18 @@ static int run_typed(lt_ctx* c, const lt_control* ctl, uint32_t modules, int64_t
     if (c->use0 < 0) return fail(LT_ERR_STATE, "no met snapshots selected (lt_met_use)");
     a.met = met_view<Rec>(c);
     if ((modules & M_MESO) && ctl->turb_meso != 0.0) {
-      // the mesoscale spreads of met0, once per met0 snapshot
-      if (!c->sig_tab) {
-        if (int rc = alloc_dev(reinterpret_cast<void**>(&c->sig_tab), 4 * sizeof(double) * n_rec(c), "spread table"))
-          return rc;
-        c->sig_slot = -1;
+      // the mesoscale spreads of met0 (built here on the compute stream if
+      // no prebuilt table describes it), then met1's prebuilt on the copy
+      // stream for the next rotation
+      int b = -1;
+      if (int rc = spread_table_for<Rec>(c, c->use0, false, &b)) return rc;
+      CK(cudaStreamWaitEvent(c->stream, c->sig_ready[b], 0));
+      a.met.sig0 = c->sig_buf[b];
+      c->meso_seen = true;
+      if (c->use1 != c->use0) {
+        int b1 = -1;
+        if (int rc = spread_table_for<Rec>(c, c->use1, true, &b1)) return rc;
       }
-      if (c->sig_slot != c->use0) {
-        CK(launch_spread_table<Rec>(a.met, c->nx, c->sig_tab, c->stream));
-        c->sig_slot = c->use0;
-      }
-      a.met.sig0 = c->sig_tab;
     }
   } else {
     std::memset(&a.met, 0, sizeof(a.met));
