@@ -517,3 +517,41 @@ def test_multi_step_launch_equals_single_steps(eng, precision, rng_mode):
         outs.append(np.stack([out.lon, out.lat, out.p, out.time]))
         e.close()
     np.testing.assert_array_equal(outs[1], outs[0])
+
+
+def test_spread_tables_follow_reloaded_slots(eng):
+    """The per-cell mesoscale spread tables are tagged by met slot: a slot
+    reloaded with new content (same slot index, same snapshot time) gets a
+    fresh table, and a prebuilt met1 table is used after the rotation —
+    both runs equal the oracle, which computes the spreads per particle."""
+    engine, ms, syn = eng
+    lons, lats, levs = syn.grid(10.0, 5.0, 20)
+    a = syn.snapshot(0.0, lons, lats, levs, syn.era5_like(lons, lats, levs, 0.0))
+    b = syn.snapshot(3600.0, lons, lats, levs, syn.era5_like(lons, lats, levs, 7.0))
+    c = syn.snapshot(0.0, lons, lats, levs, syn.era5_like(lons, lats, levs, 3.0))
+    d = syn.snapshot(7200.0, lons, lats, levs, syn.era5_like(lons, lats, levs, 11.0))
+    ctl = ms.Control(t_stop=7200.0, dt_model=600.0, rng_mode="counter", rng_seed_global=5,
+                     met_dt=3600.0, turb_meso=0.16)
+    ens = syn.particles(2000, seed=6)
+    st = {"time": ens.time.copy(), "lon": ens.lon.copy(), "lat": ens.lat.copy(),
+          "p": ens.p.copy(), "uvwp": np.zeros((3, ens.np)), "iso_var": np.zeros(ens.np),
+          "q": np.zeros((5, ens.np))}
+    mods = ("advection", "turb", "meso", "position")
+    e = engine.Engine(device=0)
+    e.upload(ens)
+    e.bind_met(a, b)
+    e.step(ctl, 0, engine.ADV_DIFF)      # tables: a (built), b (prebuilt)
+    orc.full_step(ctl, orc.Snapshot.like(a), orc.Snapshot.like(b), st, 0, ens.np, 0, modules=mods)
+    e.bind_met(c, b)                     # slot 0 now holds c: its table must be rebuilt
+    e.step(ctl, 1, engine.ADV_DIFF)
+    orc.full_step(ctl, orc.Snapshot.like(c), orc.Snapshot.like(b), st, 0, ens.np, 1, modules=mods)
+    e.prefetch(met=d)
+    e.rotate()                           # met0 = b: the prebuilt table
+    for step in (2, 3):
+        e.step(ctl, step, engine.ADV_DIFF)
+        orc.full_step(ctl, orc.Snapshot.like(b), orc.Snapshot.like(d), st, 0, ens.np, step,
+                      modules=mods)
+    got = e.download()
+    e.close()
+    for k in ("lon", "lat", "p", "time"):
+        np.testing.assert_allclose(getattr(got, k), st[k], rtol=1e-10, atol=1e-9)
