@@ -904,6 +904,11 @@ def main():
                               "philox4x32-10 keyed by (seed, step, 32-bit particle id), "
                               "in-kernel (the north star's counter-based generator)",
                        "sort_every": sort_every, "met_rotations_timed": rots,
+                       "per_snapshot_precompute": "node-pair record packing and the per-cell "
+                                                  "mesoscale spread table (2.1 ms at 0.25 deg), "
+                                                  "once per met snapshot: inside the timed region "
+                                                  "only when snapshots rotate in it "
+                                                  "(met_rotations_timed)",
                        "parallelism": f"particles sharded x{ws} ({args.scaling} scaling), met "
                                       "replicated (NCCL broadcast), no data-path collective",
                        "l2": "inputs larger than L2 (state %.1f GB/GPU, met %.1f GB)" % (

@@ -584,7 +584,7 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, step_min_blocks(FIXED, FAST, RM
         // the vertical hop moved only p: the T sample's lon/lat column holds
         const uint32_t r00 = tcol != kNoColumn ? O::cell_in_column(a.met, tcol, p)
                                                : O::cell(a.met, lon, lat, p);
-        // the AR(1) state loads go out before the spread gather so the two
+        // the AR(1) state loads go out before the spread-table load so the two
         // latencies overlap
         double prev[3];
 #pragma unroll
