@@ -438,6 +438,26 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, step_min_blocks(FIXED, FAST, RM
                              ? (a.ids ? static_cast<uint64_t>(a.ids[src]) : static_cast<uint64_t>(s))
                              : 0ull;
 
+    // the particle's index in the home-ordered row groups (one ids load,
+    // not one per row access: the row stores would keep the compiler from
+    // reusing it)
+    // (fast kernels with the isosurface / decay / meteo rows; the exact
+    // kernels re-read the id at each use — a value live across the whole
+    // iteration costs them more in spills)
+    const bool need_home = FAST != 0 && (mods & (M_ISOSURF | M_ISOSURF_INIT | M_DECAY | M_METEO));
+    const int64_t home = need_home && a.home_mask && a.ids
+                             ? static_cast<int64_t>(a.ids[src]) - a.home_base
+                             : static_cast<int64_t>(s);
+#define LT_ROW(group) (need_home ? ((a.home_mask & (group)) && a.ids ? home : static_cast<int64_t>(s)) \
+                                 : row_index(a, s, src, (group)))
+#ifndef LT_NO_L1PF_UVWP
+    // fast kernels: the decay module's q element (read late, after the
+    // gathers, from the home-ordered q rows) into L1
+    if (FAST != 0 && (mods & M_DECAY) && ctl.decay_tau > 0.0 && ctl.decay_slot >= 0 &&
+        ctl.decay_slot < a.nq)
+      prefetch_l1(a.q + static_cast<int64_t>(ctl.decay_slot) * a.cap + LT_ROW(HOME_Q));
+#endif
+
     // nsteps consecutive steps of this particle with its state in registers
     // (particles are independent within a step; the caller keeps the met
     // pair valid for all of them)
@@ -493,11 +513,11 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, step_min_blocks(FIXED, FAST, RM
       // physics.py:225-235 (module_isosurf_init)
       if ((mods & M_ISOSURF_INIT) && ctl.isosurf_mode != ISO_OFF) {
         if (ctl.isosurf_mode == ISO_PRESSURE) {
-          a.iso_var[row_index(a, s, src, HOME_ISO)] = p;
+          a.iso_var[LT_ROW(HOME_ISO)] = p;
         } else {
           double v[4];
           O::sample(a.met, time, lon, lat, p, 8, v);
-          a.iso_var[row_index(a, s, src, HOME_ISO)] = v[3] * O::power(1000.0 / p, kKappa);
+          a.iso_var[LT_ROW(HOME_ISO)] = v[3] * O::power(1000.0 / p, kKappa);
         }
         LT_CLOCK(CK_ISOSURF_INIT);
       }
@@ -632,7 +652,7 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, step_min_blocks(FIXED, FAST, RM
       // decay (new module): q[slot] *= exp(-dt / tau) while active
       if ((mods & M_DECAY) && ctl.decay_tau > 0.0 && act && ctl.decay_slot >= 0 &&
           ctl.decay_slot < a.nq) {
-        double* qs = a.q + static_cast<int64_t>(ctl.decay_slot) * a.cap + row_index(a, s, src, HOME_Q);
+        double* qs = a.q + static_cast<int64_t>(ctl.decay_slot) * a.cap + LT_ROW(HOME_Q);
         *qs = *qs * (dt == a.kc.dt ? a.kc.decay : exp(-dt / ctl.decay_tau));
         LT_CLOCK(CK_DECAY);
       }
@@ -640,9 +660,9 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, step_min_blocks(FIXED, FAST, RM
       // physics.py:238-264 (module_isosurf): applies to every particle
       if ((mods & M_ISOSURF) && ctl.isosurf_mode != ISO_OFF) {
         if (ctl.isosurf_mode == ISO_PRESSURE) {
-          p = a.iso_var[row_index(a, s, src, HOME_ISO)];
+          p = a.iso_var[LT_ROW(HOME_ISO)];
         } else {
-          const double theta0 = a.iso_var[row_index(a, s, src, HOME_ISO)];
+          const double theta0 = a.iso_var[LT_ROW(HOME_ISO)];
           nonconv += O::isosurf_theta(a.met, time, lon, lat, p, theta0) ? 0ull : 1ull;
         }
         LT_CLOCK(CK_ISOSURF);
@@ -671,7 +691,7 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, step_min_blocks(FIXED, FAST, RM
       if (mods & M_METEO) {
         double v[4];
         O::sample(a.met, time, lon, lat, p, 11, v);
-        const int64_t qi = row_index(a, s, src, HOME_Q);
+        const int64_t qi = LT_ROW(HOME_Q);
         a.q[qi] = v[3];
         a.q[a.cap + qi] = v[0];
         a.q[2 * a.cap + qi] = v[1];
@@ -705,6 +725,7 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, step_min_blocks(FIXED, FAST, RM
   }
 
 #undef LT_CLOCK
+#undef LT_ROW
   if (FIXED == 0 && clocks) {  // warp sums, one atomic per warp and module
 #pragma unroll
     for (int k = 0; k < CK_N; ++k) {
