@@ -522,7 +522,8 @@ def run_one_process(args, wl):
         for i in range(k):
             if sort_every and (st + i) % sort_every == 0:
                 e.sort(mask)
-            e.step(ctl, st + i, mask, device_id=d)
+            e.step(ctl, st + i, mask, device_id=d,
+                   sort_next=bool(sort_every) and (st + i + 1) % sort_every == 0)
         if ev:
             ev[1].record(sh)
         e.sync()
@@ -695,7 +696,8 @@ def main():
             n_sorts += 1
         if record:
             record[0].record(stream_h)
-        eng.step(c, step, mask)
+        # a sort opens the next step: this launch writes the sort keys
+        eng.step(c, step, mask, sort_next=bool(sort_every) and (step + 1) % sort_every == 0)
         if record:
             record[1].record(stream_h)
         step += 1
@@ -775,7 +777,8 @@ def main():
                     run = k_steps - done
                     if sort_every:
                         run = min(run, sort_every - st % sort_every)
-                    eng.step_many(ctl, st, run, mask)
+                    eng.step_many(ctl, st, run, mask,
+                                  sort_next=bool(sort_every) and (st + run) % sort_every == 0)
                     st += run
                     done += run
                 ev1.record(stream_h)

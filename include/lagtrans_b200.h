@@ -67,6 +67,11 @@ extern "C" {
 #define LT_RUN_MODULE_CLOCKS (1u << 3) /* fused launch charges SM cycles per module (generic
                                           kernel; read with lt_module_cycles) — the PHYSICS
                                           timer rows of driver_cli.py:151-183 / timers.py */
+#define LT_RUN_SORT_KEYS    (1u << 4) /* the launch also writes the box-sort keys of the
+                                          particles' end positions; an lt_sort_by_box of the
+                                          same range as the very next call on the context
+                                          uses them instead of computing its own (no effect
+                                          before the context's first sort) */
 
 /* rng modes (model_state.py:15 plus the fast Philox mode) */
 #define LT_RNG_FAITHFUL 0
@@ -261,6 +266,10 @@ int lt_set_home_rows(lt_ctx *ctx, uint32_t mask);
 
 /* box sort: stable radix sort of [start, end) by met0 cell, ids travel along */
 int lt_sort_by_box(lt_ctx *ctx, int64_t start, int64_t end);
+
+/* sorts run on this context, and how many of them used the keys of the
+   launch just before (LT_RUN_SORT_KEYS) instead of computing their own */
+int lt_sort_info(lt_ctx *ctx, int64_t *sorts, int64_t *sorts_with_step_keys);
 /* copies that undo the sort permutation (ids must be a permutation of
    [first_id, first_id + count)) */
 int lt_field_d2h_ordered(lt_ctx *ctx, int32_t field, int32_t row, int64_t offset,

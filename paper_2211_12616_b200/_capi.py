@@ -35,6 +35,7 @@ RUN_RNG_INKERNEL = 1 << 0
 RUN_DT_ARRAY = 1 << 1
 RUN_WRITE_DT = 1 << 2
 RUN_MODULE_CLOCKS = 1 << 3
+RUN_SORT_KEYS = 1 << 4
 # lt_module_cycles slots -> the reference's PHYSICS timer names (driver_cli.py:151-183)
 MODULE_CLOCK_NAMES = ("module_timesteps", "generate_random_nums", "module_advection",
                       "module_diffusion_turb", "module_diffusion_meso", "module_convection",
@@ -135,6 +136,7 @@ _PROTOS = {
     "lt_module_cycles": ([_P, _P, _I32], C.c_int),
     "lt_iso_counter": ([_P, C.POINTER(_I64), _I32], C.c_int),
     "lt_sort_by_box": ([_P, _I64, _I64], C.c_int),
+    "lt_sort_info": ([_P, C.POINTER(_I64), C.POINTER(_I64)], C.c_int),
     "lt_set_home_rows": ([_P, _U32], C.c_int),
     "lt_field_d2h_ordered": ([_P, _I32, _I32, _I64, _I64, _I64, _P], C.c_int),
     "lt_field_h2d_ordered": ([_P, _I32, _I32, _I64, _I64, _I64, _P], C.c_int),

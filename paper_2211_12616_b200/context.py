@@ -334,6 +334,12 @@ class DeviceContext:
     def sort_by_box(self, start: int, end: int) -> None:
         capi.check(self.lib.lt_sort_by_box(self.h, start, end))
 
+    def sort_info(self) -> tuple[int, int]:
+        """(sorts, sorts that used the keys of the step launched just before)."""
+        a, b = C.c_int64(0), C.c_int64(0)
+        capi.check(self.lib.lt_sort_info(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
     def interpolate(self, t, lon, lat, p) -> np.ndarray:
         lon = _f64(lon)
         n = lon.size

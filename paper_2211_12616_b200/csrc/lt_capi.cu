@@ -96,6 +96,16 @@ struct lt_ctx {
   uint32_t* col_rank = nullptr;  // dense rank of each Morton column code (key compression)
   int64_t col_rank_n = 0;        // its length (0: not built for the current grid)
   uint32_t col_count = 0;        // number of columns (nx * ny)
+  // the occupied level-box range of the last sort that computed its keys
+  // (the window of keys written by LT_RUN_SORT_KEYS launches)
+  bool zone_known = false;
+  uint32_t zone_min = 0, zone_max = 0;
+  // API calls on the context (check_ctx); keys written by the launch of call
+  // sk_call serve an lt_sort_by_box of [sk_start, sk_end) that is call sk_call + 1
+  uint64_t calls = 0, sk_call = ~0ull;
+  int64_t sk_start = 0, sk_end = 0;
+  uint32_t sk_nocc = 1;
+  int64_t n_sorts = 0, n_sorts_fused = 0;  // lt_sort_info
   void* cub_temp = nullptr;
   size_t cub_bytes = 0;
   unsigned long long* counters = nullptr;  // [0] iso_nonconverged, [8, 8 + CK_N) module cycles
@@ -278,8 +288,17 @@ double* field_ptr(lt_ctx* c, int field, int row, int64_t* len, int* rc) {
 
 int check_ctx(lt_ctx* c) {
   if (!c) return fail(LT_ERR_STATE, "null context (deleted region?)");
+  ++c->calls;
   CK(cudaSetDevice(c->device));
   return LT_OK;
+}
+
+// entry points that leave the particles and their slot order alone: they do
+// not count as calls between a LT_RUN_SORT_KEYS launch and its sort
+int check_ctx_keep(lt_ctx* c) {
+  const int rc = check_ctx(c);
+  if (rc == LT_OK) --c->calls;
+  return rc;
 }
 
 int check_particles(lt_ctx* c) {
@@ -431,7 +450,7 @@ int lt_ctx_destroy(lt_ctx* c) {
 }
 
 int lt_sync(lt_ctx* c) {
-  int rc = check_ctx(c);
+  int rc = check_ctx_keep(c);
   if (rc) return rc;
   CK(cudaStreamSynchronize(c->copy));
   CK(cudaStreamSynchronize(c->d2h));
@@ -583,7 +602,7 @@ static int convert_row(lt_ctx* c, double** row, bool separate, bool to_home) {
 }
 
 int lt_set_home_rows(lt_ctx* c, uint32_t mask) {
-  int rc = check_ctx(c);
+  int rc = check_ctx_keep(c);
   if (rc || (rc = check_particles(c))) return rc;
   if ((rc = settle(c))) return rc;
   if (mask & ~(LT_HOME_Q | LT_HOME_ZETA | LT_HOME_DT | LT_HOME_ISO))
@@ -633,6 +652,7 @@ int lt_met_grid(lt_ctx* c, int32_t nx, int32_t ny, int32_t nz, const double* lon
   const bool same_size = c->nx == nx && c->ny == ny && c->nz == nz && c->prec == precision;
   c->nx = nx; c->ny = ny; c->nz = nz; c->prec = precision;
   c->col_rank_n = 0;  // the key-compression table belongs to the old grid
+  c->zone_known = false;
   for (int b = 0; b < 2; ++b) {  // so do the spread tables
     free_dev(c->sig_buf[b]);
     c->sig_buf[b] = nullptr;
@@ -942,7 +962,7 @@ int lt_nccl_ranks(int32_t* nranks) {
 }
 
 int lt_met_slot_time(lt_ctx* c, int32_t slot, double* t) {
-  int rc = check_ctx(c);
+  int rc = check_ctx_keep(c);
   if (rc) return rc;
   if (slot < 0 || slot > 2) return fail(LT_ERR_ARG, "met slot outside [0, 3)");
   if (!c->slots[slot].valid) return fail(LT_ERR_STATE, "met slot %d not loaded", slot);
@@ -1039,6 +1059,37 @@ static int run_typed(lt_ctx* c, const lt_control* ctl, uint32_t modules, int64_t
   a.faithful_state = fstate; a.faithful_base = fbase;
   a.iso_nonconv = c->counters;
   a.mod_cycles = c->counters + 8;
+  a.flags &= ~F_SORT_KEYS;
+  a.sk_keys = a.sk_vals = nullptr;
+  a.sk_rank = nullptr;
+  a.sk_kmin = 0;
+  a.sk_nocc = 1;
+  a.sk_bad = nullptr;
+  bool sort_keys = false;
+  if ((flags & LT_RUN_SORT_KEYS) && !fuse_perm && c->zone_known && c->col_rank && c->sort_buf &&
+      c->col_count > 0) {
+    // the level window: as wide as the radix passes of the occupied range
+    // allow, centred on it (a particle outside it flags the keys invalid and
+    // the sort computes its own)
+    const uint32_t nlev = box_levels(c->nz);
+    const uint32_t occ = c->zone_max - c->zone_min + 1;
+    int bits = 1;
+    while (bits < 32 && (1ull << bits) <= static_cast<uint64_t>(c->col_count) * occ - 1) ++bits;
+    bits = (bits + 7) / 8 * 8;
+    const uint64_t room = bits >= 32 ? nlev : (1ull << bits) / c->col_count;
+    const uint32_t nocc = static_cast<uint32_t>(std::max<uint64_t>(occ, std::min<uint64_t>(nlev, room)));
+    uint32_t kmin = c->zone_min - std::min(c->zone_min, (nocc - occ) / 2);
+    if (kmin + nocc > nlev) kmin = nlev - nocc;
+    a.sk_keys = c->sort_buf;
+    a.sk_vals = c->sort_buf + 2 * c->cap;
+    a.sk_rank = c->col_rank;
+    a.sk_kmin = kmin;
+    a.sk_nocc = nocc;
+    a.sk_bad = reinterpret_cast<unsigned int*>(c->counters + 5);
+    CK(cudaMemsetAsync(a.sk_bad, 0, sizeof(unsigned int), c->stream));
+    a.flags |= F_SORT_KEYS;
+    sort_keys = true;
+  }
   static_assert(sizeof(lt_control) == sizeof(Control), "control layout");
   std::memcpy(&a.ctl, ctl, sizeof(Control));
   {
@@ -1091,6 +1142,14 @@ static int run_typed(lt_ctx* c, const lt_control* ctl, uint32_t modules, int64_t
     std::memset(&a.clim, 0, sizeof(a.clim));
   }
   CK(launch_step<Rec>(a, c->stream));
+  if (sort_keys) {
+    c->sk_call = c->calls;
+    c->sk_start = start;
+    c->sk_end = end;
+    c->sk_nocc = a.sk_nocc;
+  } else {
+    c->sk_call = ~0ull;
+  }
   if (fuse_perm) {  // the pool rows now hold the sorted state
     std::swap(c->time, c->pool[0]); std::swap(c->p, c->pool[1]);
     std::swap(c->lon, c->pool[2]); std::swap(c->lat, c->pool[3]);
@@ -1327,7 +1386,7 @@ int lt_rng_fill(lt_ctx* c, int32_t mode, uint64_t seed, int64_t step, int64_t st
 }
 
 int lt_module_cycles(lt_ctx* c, uint64_t* cycles, int32_t reset) {
-  int rc = check_ctx(c);
+  int rc = check_ctx_keep(c);
   if (rc) return rc;
   static_assert(CK_N <= LT_N_MODULE_CLOCKS, "clock slots");
   unsigned long long v[LT_N_MODULE_CLOCKS] = {};
@@ -1362,7 +1421,7 @@ int lt_philox4x32_10(lt_ctx* c, int32_t n, const uint32_t* ctr, const uint32_t* 
 }
 
 int lt_iso_counter(lt_ctx* c, int64_t* value, int32_t reset) {
-  int rc = check_ctx(c);
+  int rc = check_ctx_keep(c);
   if (rc) return rc;
   unsigned long long v = 0;
   CK(cudaMemcpyAsync(&v, c->counters, sizeof v, cudaMemcpyDeviceToHost, c->stream));
@@ -1464,6 +1523,24 @@ static int sort_typed(lt_ctx* c, int64_t start, int64_t end) {
                             part1by1(static_cast<uint32_t>(c->ny - 1) >> LT_BOX_SHIFT)) *
           box_levels(c->nz) + (box_levels(c->nz) - 1);
   const int morton = c->nx <= 65536 && c->ny <= 65536 && max_morton < (uint64_t(1) << 32);
+  auto nbits = [](uint64_t v) { int b = 1; while (b < 32 && (1ull << b) <= v) ++b; return b; };
+  // keys written by the step launch just before (LT_RUN_SORT_KEYS), unless a
+  // particle left their level window
+  bool fresh = morton && n > 0 && c->calls == c->sk_call + 1 && start == c->sk_start &&
+               end == c->sk_end && c->col_rank;
+  if (fresh) {
+    unsigned int bad = 1;
+    CK(cudaMemcpyAsync(&bad, c->counters + 5, sizeof bad, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    fresh = bad == 0;
+  }
+  c->sk_call = ~0ull;
+  uint64_t max_key = morton ? max_morton : static_cast<uint64_t>(n_rec(c));
+  ++c->n_sorts;
+  if (fresh) {
+    ++c->n_sorts_fused;
+    max_key = static_cast<uint64_t>(c->col_count) * c->sk_nocc - 1;
+  } else {
   unsigned int* kzone = reinterpret_cast<unsigned int*>(c->counters + 2);
   if (morton) {
     const unsigned int init[2] = {0xFFFFFFFFu, 0u};
@@ -1471,8 +1548,6 @@ static int sort_typed(lt_ctx* c, int64_t start, int64_t end) {
   }
   CK(launch_box_keys<Rec>(m, c->lon, c->lat, c->p, start, n, keys_in, vals_in, morton,
                           morton ? kzone : nullptr, c->stream));
-  uint64_t max_key = morton ? max_morton : static_cast<uint64_t>(n_rec(c));
-  auto nbits = [](uint64_t v) { int b = 1; while (b < 32 && (1ull << b) <= v) ++b; return b; };
   if (morton && n > 0) {
     // the same order in fewer key bits when that saves an 8-bit radix pass:
     // dense column ranks times the occupied level boxes (compress_keys_kernel)
@@ -1502,11 +1577,15 @@ static int sort_typed(lt_ctx* c, int64_t start, int64_t end) {
     CK(cudaMemcpyAsync(zone, kzone, sizeof zone, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     const uint32_t nocc = zone[1] - zone[0] + 1;
+    c->zone_known = true;
+    c->zone_min = zone[0];
+    c->zone_max = zone[1];
     const uint64_t max_c = static_cast<uint64_t>(c->col_count) * nocc - 1;
     if ((nbits(max_c) + 7) / 8 < (nbits(max_key) + 7) / 8) {
       CK(launch_compress_keys(keys_in, n, c->col_rank, nlev, zone[0], nocc, c->stream));
       max_key = max_c;
     }
+  }
   }
   const int bits = nbits(max_key);
   size_t need = 0;
@@ -1733,15 +1812,24 @@ int lt_group_stats(lt_ctx* c, int32_t slot, int64_t start, int64_t end, int64_t 
 
 // ------------------------------------------------------------------ timing / host memory
 
+int lt_sort_info(lt_ctx* c, int64_t* sorts, int64_t* sorts_with_step_keys) {
+  int rc = check_ctx_keep(c);
+  if (rc) return rc;
+  if (!sorts || !sorts_with_step_keys) return fail(LT_ERR_ARG, "null output");
+  *sorts = c->n_sorts;
+  *sorts_with_step_keys = c->n_sorts_fused;
+  return LT_OK;
+}
+
 int lt_timing(lt_ctx* c, int32_t enable) {
-  int rc = check_ctx(c);
+  int rc = check_ctx_keep(c);
   if (rc) return rc;
   c->timing = enable != 0;
   return LT_OK;
 }
 
 int lt_last_elapsed_ms(lt_ctx* c, float* ms) {
-  int rc = check_ctx(c);
+  int rc = check_ctx_keep(c);
   if (rc) return rc;
   if (!c->timed_once) return fail(LT_ERR_STATE, "no timed launch recorded");
   CK(cudaEventSynchronize(c->ev_stop));

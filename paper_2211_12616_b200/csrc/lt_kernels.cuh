@@ -31,34 +31,6 @@ cudaError_t launch_spread_table(const MetView<Rec>& m, int nx, double* out, cuda
 cudaError_t launch_rng_fill(int mode, uint64_t seed, int64_t step, int64_t start, int64_t end,
                             const uint32_t* ids, double* conv, double* turb, double* meso,
                             cudaStream_t st);
-// Sort key of a met cell: lon/lat columns in Z (Morton) order, levels
-// fastest within a column — neighbouring columns, whose records a cell's
-// corners share, stay close in the sorted order.
-__host__ __device__ inline uint32_t part1by1(uint32_t x) {
-  x &= 0x0000FFFFu;
-  x = (x | (x << 8)) & 0x00FF00FFu;
-  x = (x | (x << 4)) & 0x0F0F0F0Fu;
-  x = (x | (x << 2)) & 0x33333333u;
-  x = (x | (x << 1)) & 0x55555555u;
-  return x;
-}
-// Box of the sort key: one lon/lat column (LT_BOX_SHIFT coarsens it, A/B
-// only) times a pair of level cells, i.e. two consecutive records, 64 bytes,
-// half a 128-byte line (the stable sort keeps the previous order inside a
-// box).  Measured at cfg3 (ms/step incl. sorts): single level cells 5.08,
-// pairs 4.98, triples 5.14, quads 5.03, 8 cells 5.70; 2x2 columns 6.8.
-#ifndef LT_BOX_SHIFT
-#define LT_BOX_SHIFT 0
-#endif
-#ifndef LT_BOX_ZDIV
-#define LT_BOX_ZDIV 2
-#endif
-__host__ __device__ inline uint32_t box_levels(int nz) { return (nz - 2) / LT_BOX_ZDIV + 1; }
-__host__ __device__ inline uint32_t box_key_morton(int i, int j, int k, int nz) {
-  return ((part1by1(static_cast<uint32_t>(i) >> LT_BOX_SHIFT) << 1) |
-          part1by1(static_cast<uint32_t>(j) >> LT_BOX_SHIFT)) * box_levels(nz) +
-         static_cast<uint32_t>(k) / LT_BOX_ZDIV;
-}
 template <class Rec>
 cudaError_t launch_box_keys(const MetView<Rec>& m, const double* lon, const double* lat,
                             const double* p, int64_t start, int64_t n, uint32_t* keys,

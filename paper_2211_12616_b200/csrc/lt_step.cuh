@@ -62,6 +62,15 @@ struct StepArgs {
   int64_t faithful_base;
   unsigned long long* iso_nonconv;
   unsigned long long* mod_cycles;  // CK_N counters (F_MODULE_CLOCKS launches)
+  // F_SORT_KEYS: the compressed box-sort key of each particle's end position
+  // (the keys lt_sort_by_box's own box_key + compress kernels would make:
+  // rank[Morton column] * sk_nocc + (level box - sk_kmin)) into sk_keys[s -
+  // start], s - start into sk_vals; a level box outside the window sets *sk_bad
+  uint32_t* sk_keys;
+  uint32_t* sk_vals;
+  const uint32_t* sk_rank;
+  uint32_t sk_kmin, sk_nocc;
+  unsigned int* sk_bad;
   Control ctl;
   StepConst kc;
   MetView<Rec> met;
@@ -701,6 +710,27 @@ __global__ void __launch_bounds__(LT_STEP_BLOCK, step_min_blocks(FIXED, FAST, RM
       }
 
     }  // steps
+
+    // the box-sort key of the end position (a sort follows this launch)
+    if (!PERM && (a.flags & F_SORT_KEYS)) {
+      int ci, cj, ck;
+      if constexpr (FAST != 0) {
+        float fx, fy, fz;
+        ci = locate_h<FAST>(a.met.lon, lon, fx);
+        cj = locate_h<FAST>(a.met.lat, lat, fy);
+        ck = a.met.nz - 2 - locate_v<FAST>(a.met.lev, p, fz, a.met.levc);
+      } else {
+        const Cell c = cell_of(a.met, lon, lat, p);
+        ci = c.i; cj = c.j; ck = c.k;
+      }
+      const uint32_t code = (part1by1(static_cast<uint32_t>(ci) >> LT_BOX_SHIFT) << 1) |
+                            part1by1(static_cast<uint32_t>(cj) >> LT_BOX_SHIFT);
+      const uint32_t kb = static_cast<uint32_t>(ck) / LT_BOX_ZDIV - a.sk_kmin;
+      const uint32_t t = s - static_cast<uint32_t>(a.start);
+      a.sk_keys[t] = __ldg(a.sk_rank + code) * a.sk_nocc + kb;
+      a.sk_vals[t] = t;
+      if (kb >= a.sk_nocc) atomicOr(a.sk_bad, 1u);
+    }
 
     if (mods & (M_ADVECTION | M_TURB | M_MESO | M_CONVECTION | M_SEDI | M_ISOSURF | M_POSITION)) {
       st_state((PERM ? a.o_p : a.p) + s, p);

@@ -194,11 +194,16 @@ def run_simulation(ctl, ens, mets, num_devices: int = 1, *, fused: bool = True,
                         img.engine.sort(modules)
                     ctx = img.engine.ctx
                     ctx.timing(True)
+                    # a sort opens the next launch: this one writes its keys
+                    sort_next = bool(sort_every) and (step + run) % sort_every == 0 and \
+                        step + run < n_steps
                     if run > 1:
-                        img.engine.step_many(img.ctl, step, run, modules, device_id=d)
+                        img.engine.step_many(img.ctl, step, run, modules, device_id=d,
+                                             sort_next=sort_next)
                     else:
                         img.engine.step(img.ctl, step, modules, device_id=d,
-                                        num_devices=num_devices, module_clocks=module_timers)
+                                        num_devices=num_devices, module_clocks=module_timers,
+                                        sort_next=sort_next)
                     ms = ctx.last_elapsed_ms()
                     ctx.timing(False)
                     timers.record("module_fused_step", "PHYSICS", device_scope(d),

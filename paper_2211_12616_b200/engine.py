@@ -185,23 +185,26 @@ class Engine:
             self.ctx.run(ctl, capi.MOD_ISOSURF_INIT, 0, self.n)
 
     def step(self, ctl, step: int, modules: int = ADV_DIFF, device_id: int = 0,
-             num_devices: int = 1, module_clocks: bool = False) -> None:
+             num_devices: int = 1, module_clocks: bool = False, sort_next: bool = False) -> None:
         """One fused time step of every particle in the shard.  With
         module_clocks the launch also charges its SM cycles per module
-        (ctx.module_cycles; the generic, instrumented kernel runs)."""
+        (ctx.module_cycles; the generic, instrumented kernel runs).  With
+        sort_next (a box sort follows) the launch also writes the particles'
+        sort keys, which the sort then uses instead of computing its own."""
         fstate = 0
         if ctl.rng_mode == "faithful":   # the reference fills a batch every step
             if self.faithful_state is None:
                 self.faithful_state = rng_seed_for(ctl.mpi_rank, device_id)
             fstate = self.faithful_state
             self.faithful_state = advance_faithful(fstate, self.n)
-        flags = capi.RUN_RNG_INKERNEL | (capi.RUN_MODULE_CLOCKS if module_clocks else 0)
+        flags = capi.RUN_RNG_INKERNEL | (capi.RUN_MODULE_CLOCKS if module_clocks else 0) | \
+            (capi.RUN_SORT_KEYS if sort_next else 0)
         self.ctx.run(ctl, modules, 0, self.n, step=step, faithful_state=fstate,
                      faithful_base=self.first_id, flags=flags)
         self._last_modules = modules
 
     def step_many(self, ctl, step: int, nsteps: int, modules: int = ADV_DIFF,
-                  device_id: int = 0) -> None:
+                  device_id: int = 0, sort_next: bool = False) -> None:
         """`nsteps` fused steps of every particle (lt_run_steps: the
         production chain in one launch, state in registers across the steps;
         identical results).  The bound met pair must cover all of them — call
@@ -209,9 +212,11 @@ class Engine:
         (their per-step stream state lives on the host)."""
         if nsteps <= 1 or ctl.rng_mode == "faithful":
             for k in range(nsteps):
-                self.step(ctl, step + k, modules, device_id=device_id)
+                self.step(ctl, step + k, modules, device_id=device_id,
+                          sort_next=sort_next and k == nsteps - 1)
             return
-        self.ctx.run_steps(ctl, modules, 0, self.n, step, nsteps, flags=capi.RUN_RNG_INKERNEL)
+        self.ctx.run_steps(ctl, modules, 0, self.n, step, nsteps,
+                           flags=capi.RUN_RNG_INKERNEL | (capi.RUN_SORT_KEYS if sort_next else 0))
         self._last_modules = modules
 
     def step_host(self, ctl, ens, cache, step: int, modules: int = ADV_DIFF,

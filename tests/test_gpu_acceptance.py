@@ -235,9 +235,10 @@ def test_driver_multi_step_runs_equal_single_steps(m, golden_chain, monkeypatch)
 
     multi, outs_m = run()
 
-    def single(self, ctl, step, nsteps, modules=eng.ADV_DIFF, device_id=0):
+    def single(self, ctl, step, nsteps, modules=eng.ADV_DIFF, device_id=0, sort_next=False):
         for k in range(nsteps):
-            self.step(ctl, step + k, modules, device_id=device_id)
+            self.step(ctl, step + k, modules, device_id=device_id,
+                      sort_next=sort_next and k == nsteps - 1)
     monkeypatch.setattr(eng.Engine, "step_many", single)
     ref, outs_r = run()
     np.testing.assert_array_equal(multi, ref)

@@ -555,3 +555,35 @@ def test_spread_tables_follow_reloaded_slots(eng):
     e.close()
     for k in ("lon", "lat", "p", "time"):
         np.testing.assert_allclose(getattr(got, k), st[k], rtol=1e-10, atol=1e-9)
+
+
+@pytest.mark.parametrize("precision", ["exact", "fast"])
+def test_sort_with_step_keys_is_the_oracle_permutation(eng, precision):
+    """LT_RUN_SORT_KEYS: the step launched just before a sort writes the box
+    keys of the particles' end positions and the sort uses them (no key
+    kernel): the permutation is still the stable argsort of the oracle's
+    box_keys of those positions, and the fused path was taken."""
+    engine, ms, syn = eng
+    lons, lats, levs = syn.grid(2.0, 2.0, 40)
+    m0 = syn.snapshot(0.0, lons, lats, levs, syn.era5_like(lons, lats, levs, 0.0))
+    m1 = syn.snapshot(3600.0, lons, lats, levs, syn.era5_like(lons, lats, levs, 7.0))
+    ctl = ms.Control(t_stop=7200.0, dt_model=600.0, rng_mode="philox", rng_seed_global=8,
+                     met_dt=3600.0, precision=precision)
+    ens = syn.particles(30000, seed=11)
+    e = engine.Engine(device=0)
+    e.upload(ens)
+    e.bind_met(m0, m1)
+    e.sort(engine.ADV_DIFF)                     # computes its own keys (and the level window)
+    for step in range(2):
+        e.step(ctl, step, engine.ADV_DIFF)
+    ids_before = e.ctx.ids(0, ens.np).astype(np.int64)
+    e.step(ctl, 2, engine.ADV_DIFF, sort_next=True)
+    e.sort(engine.ADV_DIFF)
+    sorts, fused = e.ctx.sort_info()
+    assert (sorts, fused) == (2, 1)
+    ids_after = e.ctx.ids(0, ens.np).astype(np.int64)
+    end = e.download()                          # particle order
+    slot = ids_before - e.first_id
+    keys = orc.box_keys(orc.Snapshot.like(m0), end.lon[slot], end.lat[slot], end.p[slot])
+    np.testing.assert_array_equal(ids_after, ids_before[np.argsort(keys, kind="stable")])
+    e.close()
