@@ -707,8 +707,11 @@ def main():
         one_step(ctl)
     barrier()
 
+    fused_sorts = [0]   # sorts of the headline timed region that used step-written keys
+
     def timed(c, k_steps):
         sorts0 = n_sorts
+        info0 = eng.ctx.sort_info()[1]
         rot0 = stream["rotations"] if stream else 0
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * k_steps + 2)]
         with ClockSampler(gpu) as clk:
@@ -722,11 +725,13 @@ def main():
         kern = statistics.mean(per)
         if os.environ.get("LT_BENCH_PER_STEP"):
             print("per-step kernel ms:", " ".join(f"{t:.3f}" for t in per), file=sys.stderr)
+        fused_sorts[0] = eng.ctx.sort_info()[1] - info0
         total, kern = sharding.max_over_ranks([total, kern], dist, "cuda")
         return total, kern, clk.summary(), n_sorts - sorts0, \
             (stream["rotations"] - rot0 if stream else 0)
 
     total_ms, kern_avg, clocks, sorts_timed, rots = timed(ctl, args.steps)
+    fused_timed = fused_sorts[0]
     value = n_tot * args.steps / (total_ms / 1e3)
     b = algorithmic_bytes(cfg["chain"], work.size, nodes)
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
@@ -882,14 +887,18 @@ def main():
                          f"same {wl} met grid ({wall:.1f} s)"}
 
     # launches of our kernels in the headline timed region: one fused step
-    # per step; per sort: keys 1 + CUB radix sort 6, plus — unless every cold
-    # row is in particle order and the next step applies the permutation —
-    # row gathers (8 hot rows, plus the q rows when meteo/decay keep them in
-    # slot order, 4 per launch) + ids 1; per streamed snapshot: one packing kernel
+    # per step; per sort: CUB's histogram, scan and three onesweep passes (5),
+    # plus the key and compression kernels (2) unless the step before wrote
+    # the keys (lt_sort_info), plus — unless every cold row is in particle
+    # order and the next step applies the permutation — row gathers (8 hot
+    # rows, plus the q rows when meteo/decay keep them in slot order, 4 per
+    # launch) + ids 1; per streamed snapshot: one packing kernel, and the
+    # spread table of the new met1 when the chain has meso
     q_hot = any(m in cfg["chain"] for m in ("meteo", "decay"))
     deferred = not q_hot and "isosurf" not in cfg["chain"]
-    per_sort = 1 + 6 + (0 if deferred else 2 + (-(-ctl.nq // 4) if q_hot else 0) + 1)
-    launches = args.steps + sorts_timed * per_sort + rots
+    per_sort = 5 + (0 if deferred else 2 + (-(-ctl.nq // 4) if q_hot else 0) + 1)
+    launches = args.steps + sorts_timed * per_sort + 2 * (sorts_timed - fused_timed) + \
+        rots * (2 if "meso" in cfg["chain"] else 1)
     if rank == 0:
         print(json.dumps({
             "metric": METRIC, "value": value, "unit": "particle-steps/s", "n_gpus": ws,
@@ -906,7 +915,8 @@ def main():
                               if args.rng != "philox" else
                               "philox4x32-10 keyed by (seed, step, 32-bit particle id), "
                               "in-kernel (the north star's counter-based generator)",
-                       "sort_every": sort_every, "met_rotations_timed": rots,
+                       "sort_every": sort_every, "sorts_timed": sorts_timed,
+                       "sorts_with_step_keys": fused_timed, "met_rotations_timed": rots,
                        "per_snapshot_precompute": "node-pair record packing and the per-cell "
                                                   "mesoscale spread table (2.1 ms at 0.25 deg), "
                                                   "once per met snapshot: inside the timed region "
