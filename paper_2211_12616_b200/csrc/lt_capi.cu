@@ -1066,8 +1066,11 @@ static int run_typed(lt_ctx* c, const lt_control* ctl, uint32_t modules, int64_t
   a.sk_nocc = 1;
   a.sk_bad = nullptr;
   bool sort_keys = false;
-  if ((flags & LT_RUN_SORT_KEYS) && !fuse_perm && c->zone_known && c->col_rank && c->sort_buf &&
-      c->col_count > 0) {
+  // (the key lookup needs the met axes: launches that bind a met pair only)
+  const bool met_bound = (modules & (M_ADVECTION | M_TURB | M_MESO | M_SEDI | M_ISOSURF | M_METEO |
+                                     M_ISOSURF_INIT)) && c->use0 >= 0;
+  if ((flags & LT_RUN_SORT_KEYS) && !fuse_perm && met_bound && c->zone_known && c->col_rank &&
+      c->sort_buf && c->col_count > 0) {
     // the level window: as wide as the radix passes of the occupied range
     // allow, centred on it (a particle outside it flags the keys invalid and
     // the sort computes its own)
