@@ -587,3 +587,33 @@ def test_sort_with_step_keys_is_the_oracle_permutation(eng, precision):
     keys = orc.box_keys(orc.Snapshot.like(m0), end.lon[slot], end.lat[slot], end.p[slot])
     np.testing.assert_array_equal(ids_after, ids_before[np.argsort(keys, kind="stable")])
     e.close()
+
+
+def test_sort_with_step_keys_falls_back_outside_the_level_window(eng):
+    """Keys written by a step are used only while every particle stays in
+    the level window sized from the last sort's occupied range: convection
+    that throws particles across the column makes the sort compute its own
+    keys — and the permutation is the oracle's either way."""
+    engine, ms, syn = eng
+    lons, lats, levs = syn.grid(2.0, 2.0, 60)
+    m0 = syn.snapshot(0.0, lons, lats, levs, syn.era5_like(lons, lats, levs, 0.0))
+    m1 = syn.snapshot(3600.0, lons, lats, levs, syn.era5_like(lons, lats, levs, 5.0))
+    ctl = ms.Control(t_stop=7200.0, dt_model=600.0, rng_mode="philox", rng_seed_global=4,
+                     met_dt=3600.0, conv_prob=1.0, conv_p_top=50.0, precision="fast")
+    ens = syn.particles(20000, seed=12)
+    ens.p[:] = 500.0 + (ens.p - ens.p.mean()) * 1e-3     # one narrow level band
+    mask = engine.modules_mask(("advection", "convection", "position"))
+    e = engine.Engine(device=0)
+    e.upload(ens)
+    e.bind_met(m0, m1)
+    e.sort(mask)                                   # window from the narrow band
+    ids_before = e.ctx.ids(0, ens.np).astype(np.int64)
+    e.step(ctl, 0, mask, sort_next=True)           # convection: p anywhere in [50, p_surf]
+    e.sort(mask)
+    assert e.ctx.sort_info() == (2, 0)
+    ids_after = e.ctx.ids(0, ens.np).astype(np.int64)
+    end = e.download()
+    slot = ids_before - e.first_id
+    keys = orc.box_keys(orc.Snapshot.like(m0), end.lon[slot], end.lat[slot], end.p[slot])
+    np.testing.assert_array_equal(ids_after, ids_before[np.argsort(keys, kind="stable")])
+    e.close()
